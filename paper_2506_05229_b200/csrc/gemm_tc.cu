@@ -1,0 +1,538 @@
+// tcgen05 / TMEM / TMA grouped GEMM for sm_100a (bf16 in, fp32 accumulate).
+//
+// Replaces the reference's grouped_gemm (armt/tensor_ops.py:237-264): every
+// matmul of a diagonal step (QKV, O, gate/up, down, memory projections,
+// associative read, LM head) is ONE launch over all members of the step, each
+// member using its own layer's weights via per-member (slot, layer) tables that
+// become TMA coordinates.
+//
+// Structure (one CTA per SM, persistent over tiles, 256 threads):
+//   warp 0      TMA producer: A tile (128 x 64) + B tile (BN x 64) per stage,
+//               128B-swizzled, signalled on a full mbarrier (expect_tx).
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=BN, K=16)
+//               x4 per stage into a TMEM accumulator; tcgen05.commit frees the
+//               stage; the last k-block commits "accumulator full".
+//   warp 2      TMEM allocator (2 accumulators x BN columns, double buffered
+//               so the epilogue of tile i overlaps the mainloop of tile i+1).
+//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 cols -> registers -> fused
+//               epilogue (residual / guarded retrieve / SwiGLU / RoPE) -> HBM.
+//
+// Tiles are ordered (member, n-block, m-block) with m fastest, so the CTAs in
+// flight share a few weight tiles (read once from HBM) and the member's
+// activation (L2-resident).
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <vector>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace armt {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NUM_THREADS = 256;
+
+struct Params {
+  int G, M, N, K;
+  int tiles_m, tiles_n, num_tiles, k_blocks;
+  int c_dtype;
+  void* C; long long ldc, c_stride;
+  const float* R; long long ldr, r_stride;
+  __nv_bfloat16* C2; long long ldc2, c2_stride;
+  const float* den; long long den_stride;
+  float eps;
+  const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
+  int swiglu_block;
+  short a_slot[ARMT_MAX_MEMBERS];
+  short b_index[ARMT_MAX_MEMBERS];
+  short c_slot[ARMT_MAX_MEMBERS];
+};
+
+template <int BN> struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+        "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled operand tile: 8-row x 128B atoms stacked every 1024 B.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4)      // start address
+         | ((uint64_t)0 << 16)                    // leading byte offset (unused, single atom in K)
+         | ((uint64_t)(1024 >> 4) << 32)          // stride byte offset: next 8-row group
+         | ((uint64_t)1 << 46)                    // sm100 descriptor version
+         | ((uint64_t)2 << 61);                   // SWIZZLE_128B
+}
+
+// kind::f16 instruction descriptor: D=f32, A=B=bf16, both K-major, M=128, N=BN.
+template <int BN> __device__ __forceinline__ constexpr uint32_t instr_desc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- epilogues
+enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4 };
+
+// Store 32 consecutive values of one row starting at column n0 (< N).
+__device__ __forceinline__ void store_row32(void* base, int dtype, long long off, int n0, int N,
+                                            long long ld, const float (&v)[32]) {
+  const int cnt = min(32, N - n0);
+  if (dtype == ARMT_BF16) {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + off + n0;
+    if (cnt == 32 && ((ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        q[j] = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                          pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < cnt) p[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* p = reinterpret_cast<float*>(base) + off + n0;
+    if (cnt == 32 && ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < cnt) p[j] = v[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void load_row32_f32(const float* p, int cnt, bool vec, float (&v)[32]) {
+  if (cnt == 32 && vec) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 t = q[j];
+      v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = j < cnt ? p[j] : 0.f;
+  }
+}
+
+// RoPE over one chunk of CH (>= DH, multiple of DH) columns held in registers.
+// Pairs (i, i + DH/2) inside each head; position = row within the segment.
+template <int DH, int CH>
+__device__ __forceinline__ void rope_chunk(float (&x)[CH], const float* cos_row, const float* sin_row) {
+  constexpr int H2 = DH / 2;
+#pragma unroll
+  for (int h = 0; h < CH / DH; ++h) {
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      const float c = cos_row[i], s = sin_row[i];
+      const float a = x[h * DH + i], b = x[h * DH + i + H2];
+      x[h * DH + i] = a * c - b * s;
+      x[h * DH + i + H2] = b * c + a * s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <int BN, int EPI, int DH>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ Params p) {
+  using C = Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(C::TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles_mn = p.tiles_m * p.tiles_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0; uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int g = tile / tiles_mn, r = tile - g * tiles_mn;
+        const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
+        const int a_slot = p.a_slot[g], b_idx = p.b_index[g];
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM, a_slot);
+          tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN, b_idx);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = instr_desc<BN>();
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a_desc = smem_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t b_desc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+            mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        acc ^= 1; if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31
+    const int ew = warp & 3;
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int g = tile / tiles_mn, r = tile - g * tiles_mn;
+      const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
+      const int row = mb * BM + ew * 32 + lane;
+      const bool live = row < p.M;
+      const int c_slot = p.c_slot[g];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+
+      if constexpr (EPI == E_SWIGLU) {
+        const int out_n0 = nb * (BN / 2);
+        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+          float gte[32], up[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, gte);
+          tmem_ld32(tbase + BN / 2 + c0, up);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gte[j] = silu_ref(gte[j]) * up[j];
+          if (live && out_n0 + c0 < p.N / 2) store_row32(p.C, ARMT_BF16, off, out_n0 + c0, p.N / 2, p.ldc, gte);
+        }
+      } else if constexpr (EPI == E_ROPE) {
+        constexpr int CH = DH > 32 ? DH : 32;
+        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
+        const float* cos_row = p.rope_cos + (long long)(live ? row : 0) * (DH / 2);
+        const float* sin_row = p.rope_sin + (long long)(live ? row : 0) * (DH / 2);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += CH) {
+          float x[CH];
+#pragma unroll
+          for (int q = 0; q < CH / 32; ++q) {
+            float t[32];
+            __syncwarp();
+            tmem_ld32(tbase + c0 + 32 * q, t);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[32 * q + j] = t[j];
+          }
+          const int n0 = nb * BN + c0;
+          if (live && n0 < p.N) {
+            if (n0 < p.rope_cols) rope_chunk<DH, CH>(x, cos_row, sin_row);
+#pragma unroll
+            for (int q = 0; q < CH / 32; ++q) {
+              float t[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) t[j] = x[32 * q + j];
+              if (n0 + 32 * q < p.N) store_row32(p.C, ARMT_BF16, off, n0 + 32 * q, p.N, p.ldc, t);
+            }
+          }
+        }
+      } else {
+        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
+        float den = 1.f; bool guarded = false;
+        if constexpr (EPI == E_RETRIEVE) {
+          if (live) den = p.den[(long long)g * p.den_stride + row];
+          guarded = fabsf(den) <= p.eps;
+        }
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          const int n0 = nb * BN + c0;
+          if (!live || n0 >= p.N) continue;  // after the warp-wide load: safe
+          if constexpr (EPI == E_RESIDUAL || EPI == E_RETRIEVE) {
+            const float* rp = p.R + (long long)c_slot * p.r_stride + (long long)row * p.ldr + n0;
+            float res[32];
+            load_row32_f32(rp, min(32, p.N - n0),
+                           ((p.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0), res);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if constexpr (EPI == E_RETRIEVE) v[j] = res[j] + (guarded ? 0.f : v[j] / den);
+              else v[j] = res[j] + v[j];
+            }
+            store_row32(p.C, ARMT_F32, off, n0, p.N, p.ldc, v);
+            if (EPI == E_RESIDUAL && p.C2 != nullptr)
+              store_row32(p.C2, ARMT_BF16, (long long)c_slot * p.c2_stride + (long long)row * p.ldc2,
+                          n0, p.N, p.ldc2, v);
+          } else {
+            store_row32(p.C, p.c_dtype, off, n0, p.N, p.ldc, v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1; if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS) : "memory");
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3D bf16 map: (cols=K contiguous, rows, batch) with a (64, box_rows, 1) box, 128B swizzle.
+static int make_map(CUtensorMap* map, const void* base, long long cols, long long rows,
+                    long long batches, long long ld, long long batch_stride, int box_rows) {
+  auto encode = get_encode();
+  ARMT_REQUIRE(encode != nullptr, ARMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  ARMT_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, ARMT_ERR_DIM, "TMA base not 16B aligned");
+  ARMT_REQUIRE((ld * 2) % 16 == 0 && (batch_stride * 2) % 16 == 0, ARMT_ERR_DIM,
+               "TMA strides must be multiples of 16 bytes (ld=%lld, batch=%lld)", ld, batch_stride);
+  if (batches == 1) batch_stride = rows * ld;  // unused dimension; any legal stride
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batches};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(batch_stride * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ARMT_REQUIRE(r == CUDA_SUCCESS, ARMT_ERR_DIM, "cuTensorMapEncodeTiled failed (%d): cols=%lld rows=%lld batches=%lld ld=%lld",
+               (int)r, cols, rows, batches, ld);
+  return ARMT_OK;
+}
+
+template <int BN, int EPI, int DH>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
+  auto kern = gemm_kernel<BN, EPI, DH>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM_BYTES);
+    attr_done = true;
+  }
+  const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+  kern<<<grid, NUM_THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ma, mb, p);
+  ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
+  return ARMT_OK;
+}
+
+static int pick_bn(const ArmtGemmArgs& a) {
+  if (a.epilogue == ARMT_EPI_SWIGLU) return 2 * a.swiglu_block;
+  const int sms = num_sms();
+  const long long tm = (a.M + BM - 1) / BM;
+  const bool rope = a.epilogue == ARMT_EPI_ROPE;
+  int best = rope ? 128 : 64;
+  double best_score = -1.0;
+  for (int bn : {256, 128, 64}) {
+    if (rope && (bn < 128 || bn % a.head_dim != 0)) continue;
+    const long long tn = (a.N + bn - 1) / bn;
+    const long long tiles = (long long)a.G * tm * tn;
+    const long long waves = (tiles + sms - 1) / sms;
+    const double fill = (double)tiles / (double)(waves * sms);      // wave quantisation
+    const double useful = (double)a.N / (double)(tn * bn);          // N padding
+    const double size = bn == 256 ? 1.0 : bn == 128 ? 0.93 : 0.8;   // per-tile efficiency
+    const double score = fill * useful * size;
+    if (score > best_score + 1e-9) { best_score = score; best = bn; }
+  }
+  return best;
+}
+
+template <int BN>
+static int dispatch_epi(const ArmtGemmArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+                        cudaStream_t s) {
+  switch (a.epilogue) {
+    case ARMT_EPI_STORE: return launch<BN, E_STORE, 0>(ma, mb, p, s);
+    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0>(ma, mb, p, s);
+    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0>(ma, mb, p, s);
+    case ARMT_EPI_SWIGLU:
+      if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0>(ma, mb, p, s);
+      break;
+    case ARMT_EPI_ROPE:
+      if constexpr (BN >= 128) {
+        switch (a.head_dim) {
+          case 8: return launch<BN, E_ROPE, 8>(ma, mb, p, s);
+          case 16: return launch<BN, E_ROPE, 16>(ma, mb, p, s);
+          case 32: return launch<BN, E_ROPE, 32>(ma, mb, p, s);
+          case 64: return launch<BN, E_ROPE, 64>(ma, mb, p, s);
+          case 128: return launch<BN, E_ROPE, 128>(ma, mb, p, s);
+          default: break;
+        }
+      }
+      break;
+  }
+  set_error("tcgen05 gemm: unsupported epilogue %d / BN %d / head_dim %d", a.epilogue, BN, a.head_dim);
+  return ARMT_ERR_UNSUPPORTED;
+}
+
+}  // namespace tc
+
+int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
+  using namespace tc;
+  ARMT_REQUIRE(a.K % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs K %% 8 == 0 (K=%d)", a.K);
+  ARMT_REQUIRE(a.lda % 8 == 0 && a.ldb % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs lda/ldb %% 8 == 0");
+  if (a.epilogue == ARMT_EPI_SWIGLU)
+    ARMT_REQUIRE((a.swiglu_block == 32 || a.swiglu_block == 128) && a.N % (2 * a.swiglu_block) == 0,
+                 ARMT_ERR_UNSUPPORTED, "SwiGLU block must be 32 or 128 and divide N/2");
+  const int bn = pick_bn(a);
+  int max_a = 0, max_b = 0;
+  for (int g = 0; g < a.G; ++g) {
+    max_a = a.a_slot[g] > max_a ? a.a_slot[g] : max_a;
+    max_b = a.b_index[g] > max_b ? a.b_index[g] : max_b;
+  }
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, bn);
+  if (rc) return rc;
+
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.G = a.G; p.M = a.M; p.N = a.N; p.K = a.K;
+  p.tiles_m = (a.M + BM - 1) / BM;
+  p.tiles_n = (a.N + bn - 1) / bn;
+  p.num_tiles = a.G * p.tiles_m * p.tiles_n;
+  p.k_blocks = (a.K + BK - 1) / BK;
+  p.c_dtype = a.c_dtype;
+  p.C = a.C; p.ldc = a.ldc; p.c_stride = a.c_stride;
+  p.R = a.R; p.ldr = a.ldr; p.r_stride = a.r_stride;
+  p.C2 = reinterpret_cast<__nv_bfloat16*>(a.C2); p.ldc2 = a.ldc2; p.c2_stride = a.c2_stride;
+  p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
+  p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
+  p.swiglu_block = a.swiglu_block;
+  for (int g = 0; g < a.G; ++g) {
+    p.a_slot[g] = (short)a.a_slot[g];
+    p.b_index[g] = (short)a.b_index[g];
+    p.c_slot[g] = (short)a.c_slot[g];
+  }
+  switch (bn) {
+    case 64: return dispatch_epi<64>(a, ma, mb, p, s);
+    case 128: return dispatch_epi<128>(a, ma, mb, p, s);
+    case 256: return dispatch_epi<256>(a, ma, mb, p, s);
+  }
+  return ARMT_ERR_UNSUPPORTED;
+}
+
+}  // namespace armt

@@ -1,0 +1,476 @@
+"""Device-resident weights, memory state and the per-step kernel sequence.
+
+``Engine.step`` is the B200 replacement for one pass of the reference's
+stacked cores (armt/executors.py:200-203): retrieve_stack -> forward_stack ->
+update_stack for G (slot, layer) members in ONE grouped launch per op. The
+executors (``executors.py``) drive it along the wavefront; the public
+per-core functions (``memory.py``, ``layers.py``) are thin wrappers.
+
+HBM layout
+  weights   K-major (out, in) per layer, layer-stacked, bf16 (or f32 in the
+            parity mode): wqkv (L, 3d, d), wo (L, d, d), wgu (L, 2F, d) with
+            gate/up interleaved in blocks of ``swiglu_block`` columns, wdown
+            (L, d, F), wqa (L, d_mem, d), wkvb (L, Nkvb, d) = [W_v; W_k; W_beta; 0],
+            unemb (V, d). F = d_ff padded to a multiple of 32 (zero rows/cols).
+  state     A (L, d, d_phi) f32, z (L, d_phi) f32 — the reference MemoryState
+            shapes — plus a bf16 shadow of A (L, d, d_phi_pad) for tensor-core
+            retrieval, refreshed by the fold kernel.
+  slots     residual stream per in-flight segment: xs (n_slots, T, d) f32 and,
+            in bf16 mode, its bf16 copy xs_bf written by the same epilogues.
+  members   per-step temporaries stacked over members: h, qkv, ctx, gu, q, phi,
+            den, kvb.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BF16, F32, EPI_RESIDUAL, EPI_RETRIEVE, EPI_ROPE, EPI_STORE, EPI_SWIGLU
+from .config import ModelConfig, ROPE_BASE, resolve_dtype
+from .errors import DimensionError, InputError
+from .weights import GroupedWeights, expected_shapes
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+# ============================================================================
+# Prepared weights
+# ============================================================================
+
+@dataclass
+class PreparedWeights:
+    """Device weights in kernel layouts (armt/layers.py:54-134 counterpart)."""
+
+    config: ModelConfig
+    dtype_name: str
+    eps_assoc: float
+    device: torch.device
+    wdtype: torch.dtype
+    T: int
+    d_head: int
+    d_phi: int
+    d_phi_pad: int
+    d_ff_pad: int
+    swiglu_block: int
+    n_kvb: int
+    embedding: torch.Tensor
+    mem_embedding: torch.Tensor
+    wqkv: torch.Tensor
+    wo: torch.Tensor
+    wgu: torch.Tensor
+    wdown: torch.Tensor
+    attn_gain: torch.Tensor
+    mlp_gain: torch.Tensor
+    wqa: torch.Tensor
+    wkvb: torch.Tensor
+    unemb: torch.Tensor
+    rope_cos: torch.Tensor
+    rope_sin: torch.Tensor
+
+    @property
+    def ab(self) -> int:
+        return BF16 if self.dtype_name == "bf16" else F32
+
+    @property
+    def v_off(self) -> int:
+        return 0
+
+    @property
+    def k_off(self) -> int:
+        return self.config.d_model
+
+    @property
+    def b_off(self) -> int:
+        return self.config.d_model + self.config.d_mem
+
+
+def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=None,
+                    layers: range | None = None) -> PreparedWeights:
+    """Cast, transpose to K-major, pad and upload (one-time setup).
+
+    ``layers`` restricts the per-layer tensors to a contiguous block (layer
+    sharding); layer indices stay global in the executors and are rebased here.
+    """
+    cfg = weights.config
+    resolve_dtype(dtype_name)
+    for name, shape in expected_shapes(cfg).items():
+        got = np.shape(getattr(weights, name))
+        if tuple(got) != shape:
+            raise InputError(f"weight tensor {name!r} has shape {got}, config expects {shape}")
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+        raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    bf16 = dtype_name == "bf16"
+    wdt = torch.bfloat16 if bf16 else torch.float32
+    L, d, dff, dm = cfg.n_layers, cfg.d_model, cfg.d_ff, cfg.d_mem
+    lo, hi = (0, L) if layers is None else (layers.start, layers.stop)
+    if bf16 and d % 8:
+        raise DimensionError("bf16 path needs d_model % 8 == 0 (TMA 16-byte rows)")
+    dh = cfg.d_head
+    T = cfg.tokens_per_segment
+    d_phi = cfg.d_phi
+    d_phi_pad = _round_up(d_phi, 8) if bf16 else d_phi
+    d_ff_pad = _round_up(dff, 32)
+    block = 128 if d_ff_pad % 128 == 0 else 32
+    n_kvb = _round_up(d + dm + 1, 16)
+
+    def up(name, sl=True):
+        a = getattr(weights, name)
+        a = a[lo:hi] if sl else a
+        return torch.as_tensor(np.ascontiguousarray(a)).to(dev, torch.float32)
+
+    def kmajor(t):  # (L, in, out) -> (L, out, in)
+        return t.transpose(1, 2).contiguous()
+
+    wqkv = kmajor(torch.cat([up("wq"), up("wk"), up("wv")], dim=2)).to(wdt)
+    wo = kmajor(up("wo")).to(wdt)
+    Ls = hi - lo
+    gate = torch.zeros(Ls, d, d_ff_pad, device=dev)
+    upw = torch.zeros(Ls, d, d_ff_pad, device=dev)
+    gate[:, :, :dff] = up("w_gate")
+    upw[:, :, :dff] = up("w_in")
+    nt = d_ff_pad // block
+    gu = torch.stack([gate.view(Ls, d, nt, block), upw.view(Ls, d, nt, block)], dim=3)
+    wgu = kmajor(gu.reshape(Ls, d, 2 * d_ff_pad)).to(wdt)
+    del gate, upw, gu
+    wout = torch.zeros(Ls, d_ff_pad, d, device=dev)
+    wout[:, :dff] = up("w_out")
+    wdown = kmajor(wout).to(wdt)
+    del wout
+    wkvb = torch.zeros(Ls, n_kvb, d, device=dev)
+    wkvb[:, :d] = up("w_v_mem")
+    wkvb[:, d:d + dm] = up("w_k_mem")
+    wkvb[:, d + dm] = up("w_beta")[:, 0]
+    inv = ROPE_BASE ** (-np.arange(0, dh, 2, dtype=np.float64) / dh)
+    ang = np.arange(T, dtype=np.float64)[:, None] * inv[None, :]
+    prepared = PreparedWeights(
+        config=cfg, dtype_name=dtype_name, eps_assoc=cfg.effective_eps_assoc(dtype_name),
+        device=dev, wdtype=wdt, T=T, d_head=dh, d_phi=d_phi, d_phi_pad=d_phi_pad,
+        d_ff_pad=d_ff_pad, swiglu_block=block, n_kvb=n_kvb,
+        embedding=up("embedding", False).to(wdt), mem_embedding=up("mem_embedding", False).to(wdt),
+        wqkv=wqkv, wo=wo, wgu=wgu, wdown=wdown,
+        attn_gain=up("attn_gain").contiguous(), mlp_gain=up("mlp_gain").contiguous(),
+        wqa=up("w_q_assoc").to(wdt).contiguous(), wkvb=wkvb.to(wdt),
+        unemb=up("unembedding", False).t().contiguous().to(wdt),
+        rope_cos=torch.as_tensor(np.cos(ang), dtype=torch.float32).to(dev).contiguous(),
+        rope_sin=torch.as_tensor(np.sin(ang), dtype=torch.float32).to(dev).contiguous(),
+    )
+    prepared.layer_base = lo
+    torch.cuda.synchronize(dev)
+    return prepared
+
+
+# ============================================================================
+# Memory state
+# ============================================================================
+
+@dataclass
+class MemoryState:
+    """Per-layer fast weights on device (armt/memory.py:52-87).
+
+    A (L, d, d_phi) f32, z (L, d_phi) f32 (fp32 in both device precisions),
+    updates (L,) int64 on the host (pure bookkeeping). ``shadow`` is the
+    bf16 copy of A the tensor-core retrieval reads; it is derived state.
+    """
+
+    A: torch.Tensor
+    z: torch.Tensor
+    updates: np.ndarray
+    shadow: torch.Tensor | None = field(default=None, repr=False)
+
+    @classmethod
+    def fresh(cls, config: ModelConfig, device=None, n_layers: int | None = None) -> "MemoryState":
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        L = config.n_layers if n_layers is None else n_layers
+        return cls(A=torch.zeros(L, config.d_model, config.d_phi, device=dev),
+                   z=torch.zeros(L, config.d_phi, device=dev),
+                   updates=np.zeros(L, np.int64))
+
+    @classmethod
+    def from_numpy(cls, A, z, updates, device=None) -> "MemoryState":
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        return cls(A=torch.as_tensor(np.asarray(A, np.float32)).to(dev).contiguous(),
+                   z=torch.as_tensor(np.asarray(z, np.float32)).to(dev).contiguous(),
+                   updates=np.array(updates, np.int64))
+
+    def clone(self) -> "MemoryState":
+        return MemoryState(self.A.clone(), self.z.clone(), self.updates.copy())
+
+    def to_numpy(self):
+        return self.A.float().cpu().numpy(), self.z.float().cpu().numpy(), self.updates.copy()
+
+    def check_compatible(self, prepared: PreparedWeights, n_layers: int | None = None) -> None:
+        cfg = prepared.config
+        L = cfg.n_layers if n_layers is None else n_layers
+        want = (L, cfg.d_model, cfg.d_phi)
+        if tuple(self.A.shape) != want or tuple(self.z.shape) != (L, cfg.d_phi):
+            raise InputError(f"memory state shaped {tuple(self.A.shape)}/{tuple(self.z.shape)}, "
+                             f"config expects {want}/{(L, cfg.d_phi)}")
+        if self.A.dtype != torch.float32 or self.z.dtype != torch.float32:
+            raise InputError("memory state must be float32 on the device path")
+        if self.A.device != prepared.device:
+            raise InputError(f"memory state on {self.A.device}, weights on {prepared.device}")
+        if not (self.A.is_contiguous() and self.z.is_contiguous()):
+            raise InputError("memory state tensors must be contiguous")
+
+    def sync_shadow(self, prepared: PreparedWeights) -> None:
+        """(Re)build the bf16 copy of A read by tensor-core retrieval (setup
+        work at run start, on the current stream; the fold kernel keeps it
+        in sync afterwards)."""
+        if prepared.dtype_name != "bf16":
+            return
+        L, d, dphi = self.A.shape
+        if self.shadow is None or tuple(self.shadow.shape) != (L, d, prepared.d_phi_pad):
+            self.shadow = torch.zeros(L, d, prepared.d_phi_pad, dtype=torch.bfloat16, device=self.A.device)
+        self.shadow[:, :, :dphi].copy_(self.A)
+
+
+# ============================================================================
+# Engine: workspace + one wavefront step
+# ============================================================================
+
+class Engine:
+    """Kernel sequence for one schedule step over G members.
+
+    ``n_slots`` activation slots hold the residual stream of in-flight
+    segments; member g of a step is (slots[g], layers[g]). ``layers`` are
+    global layer indices; weights/state may hold only a contiguous block
+    starting at ``layer_base`` (layer sharding).
+    """
+
+    def __init__(self, prepared: PreparedWeights, max_members: int, n_slots: int,
+                 n_state_layers: int | None = None):
+        p = prepared
+        cfg = p.config
+        self.p = p
+        self.cfg = cfg
+        self.lib = _lib.load()
+        self.max_members = max_members
+        self.n_slots = n_slots
+        self.layer_base = getattr(p, "layer_base", 0)
+        dev = p.device
+        T, d, G = p.T, cfg.d_model, max_members
+        wdt = p.wdtype
+        self.bf16 = p.dtype_name == "bf16"
+        self.xs = torch.zeros(n_slots, T, d, device=dev)
+        self.xs_bf = torch.zeros(n_slots, T, d, dtype=torch.bfloat16, device=dev) if self.bf16 else None
+        self.h = torch.empty(G, T, d, dtype=wdt, device=dev)
+        self.qkv = torch.empty(G, T, 3 * d, dtype=wdt, device=dev)
+        self.ctx = torch.empty(G, T, d, dtype=wdt, device=dev)
+        self.gu = torch.empty(G, T, p.d_ff_pad, dtype=wdt, device=dev)
+        self.gu_full = None if self.bf16 else torch.empty(G, T, 2 * p.d_ff_pad, dtype=wdt, device=dev)
+        self.qm = torch.empty(G, T, cfg.d_mem, device=dev)
+        self.phi = torch.zeros(G, T, p.d_phi_pad, dtype=wdt, device=dev)
+        self.den = torch.empty(G, T, device=dev)
+        self.kvb = torch.empty(G, cfg.num_mem_tokens, p.n_kvb, device=dev)
+        nb = int(self.lib.armt_fold_workspace_bytes(G, cfg.num_mem_tokens, p.d_phi))
+        self.fold_ws = torch.empty(max(nb, 16) // 4 + 1, device=dev)
+        self._cache: dict = {}
+        self.launches_per_step = 12
+
+    # -- argument builders (memoised: graphs/eager replays reuse the structs) --
+    def _gemm(self, key, fill):
+        args = self._cache.get(key)
+        if args is None:
+            args = _lib.ArmtGemmArgs()
+            fill(args)
+            self._cache[key] = args
+        return args
+
+    def _members(self, slots, layers):
+        key = ("mem", tuple(slots), tuple(layers))
+        m = self._cache.get(key)
+        if m is None:
+            m = _lib.members(slots, [l - self.layer_base for l in layers])
+            self._cache[key] = m
+        return m
+
+    @staticmethod
+    def _tables(args, a_slots, b_index, c_slots):
+        args.G = len(b_index)
+        for g in range(args.G):
+            args.a_slot[g] = int(a_slots[g])
+            args.b_index[g] = int(b_index[g])
+            args.c_slot[g] = int(c_slots[g])
+
+    # -- embedding boundary ---------------------------------------------------
+    def embed(self, ids: torch.Tensor, slot: int, stream: int) -> None:
+        """armt/layers.py:306-318 into activation slot ``slot``."""
+        p, cfg = self.p, self.cfg
+        T, d = p.T, cfg.d_model
+        xb = None if self.xs_bf is None else self.xs_bf[slot].data_ptr()
+        _lib.check(self.lib.armt_embed(ids.data_ptr(), p.embedding.data_ptr(), p.mem_embedding.data_ptr(),
+                                       p.ab, self.xs[slot].data_ptr(), xb, cfg.segment_size,
+                                       cfg.num_mem_tokens, d, cfg.vocab_size, stream), "embed")
+
+    # -- the three stacked cores ---------------------------------------------
+    def retrieve(self, slots, layers, state: MemoryState, stream: int) -> None:
+        """retrieve_stack (armt/memory.py:132-152), in place on xs[slots]."""
+        p, cfg, lib = self.p, self.cfg, self.lib
+        T, d, G = p.T, cfg.d_model, len(layers)
+        lrel = [l - self.layer_base for l in layers]
+        gid = list(range(G))
+        src = self.xs_bf if self.bf16 else self.xs
+
+        def fill_q(a):
+            a.M, a.N, a.K, a.ab_dtype = T, cfg.d_mem, d, p.ab
+            a.A, a.lda, a.a_stride = src.data_ptr(), d, T * d
+            a.B, a.ldb, a.b_stride = p.wqa.data_ptr(), d, cfg.d_mem * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.qm.data_ptr(), cfg.d_mem, T * cfg.d_mem, F32
+            a.epilogue = EPI_STORE
+            self._tables(a, slots, lrel, gid)
+        args = self._gemm(("q", tuple(slots), tuple(layers)), fill_q)
+        _lib.check(lib.armt_gemm(args, stream), "retrieve q-proj")
+        mem = self._members(slots, layers)
+        _lib.check(lib.armt_dpfp_den(mem, self.qm.data_ptr(), T * cfg.d_mem, state.z.data_ptr(),
+                                     self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
+                                     self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
+        bmat = state.shadow if self.bf16 else state.A
+        ld_b = p.d_phi_pad if self.bf16 else p.d_phi
+
+        def fill_n(a):
+            a.M, a.N, a.K, a.ab_dtype = T, d, ld_b, p.ab
+            a.A, a.lda, a.a_stride = self.phi.data_ptr(), p.d_phi_pad, T * p.d_phi_pad
+            a.B, a.ldb, a.b_stride = bmat.data_ptr(), ld_b, d * ld_b
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.xs.data_ptr(), d, T * d, F32
+            a.epilogue = EPI_RETRIEVE
+            a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
+            a.den, a.den_stride, a.eps = self.den.data_ptr(), T, p.eps_assoc
+            self._tables(a, gid, lrel, slots)
+        args = self._gemm(("num", tuple(slots), tuple(layers), bmat.data_ptr()), fill_n)
+        _lib.check(lib.armt_gemm(args, stream), "retrieve numerator")
+
+    def forward(self, slots, layers, stream: int) -> None:
+        """forward_stack (armt/layers.py:235-246), in place on xs[slots]."""
+        p, cfg, lib = self.p, self.cfg, self.lib
+        T, d, G = p.T, cfg.d_model, len(layers)
+        lrel = [l - self.layer_base for l in layers]
+        gid = list(range(G))
+        key = (tuple(slots), tuple(layers))
+        mem = self._members(slots, layers)
+        wout = BF16 if self.bf16 else F32
+        # attention sub-block
+        _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.attn_gain.data_ptr(), self.h.data_ptr(),
+                                    wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm attn")
+
+        def fill_qkv(a):
+            a.M, a.N, a.K, a.ab_dtype = T, 3 * d, d, p.ab
+            a.A, a.lda, a.a_stride = self.h.data_ptr(), d, T * d
+            a.B, a.ldb, a.b_stride = p.wqkv.data_ptr(), d, 3 * d * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.qkv.data_ptr(), 3 * d, T * 3 * d, wout
+            if self.bf16:
+                a.epilogue = EPI_ROPE
+                a.rope_cos, a.rope_sin = p.rope_cos.data_ptr(), p.rope_sin.data_ptr()
+                a.head_dim, a.rope_cols = p.d_head, 2 * d
+            else:
+                a.epilogue = EPI_STORE
+            self._tables(a, gid, lrel, gid)
+        _lib.check(lib.armt_gemm(self._gemm(("qkv",) + key, fill_qkv), stream), "qkv")
+        if not self.bf16:
+            _lib.check(lib.armt_rope(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, F32, T, cfg.n_heads, p.d_head,
+                                     p.rope_cos.data_ptr(), p.rope_sin.data_ptr(), stream), "rope")
+        _lib.check(lib.armt_attention(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, self.ctx.data_ptr(), d, T * d,
+                                      wout, T, cfg.n_heads, p.d_head, 1.0 / math.sqrt(p.d_head), stream),
+                   "attention")
+
+        def fill_o(a):
+            a.M, a.N, a.K, a.ab_dtype = T, d, d, p.ab
+            a.A, a.lda, a.a_stride = self.ctx.data_ptr(), d, T * d
+            a.B, a.ldb, a.b_stride = p.wo.data_ptr(), d, d * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.xs.data_ptr(), d, T * d, F32
+            a.epilogue = EPI_RESIDUAL
+            a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
+            self._tables(a, gid, lrel, slots)
+        _lib.check(lib.armt_gemm(self._gemm(("o",) + key, fill_o), stream), "o-proj")
+        # MLP sub-block
+        _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.mlp_gain.data_ptr(), self.h.data_ptr(),
+                                    wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm mlp")
+        F = p.d_ff_pad
+
+        def fill_gu(a):
+            a.M, a.N, a.K, a.ab_dtype = T, 2 * F, d, p.ab
+            a.A, a.lda, a.a_stride = self.h.data_ptr(), d, T * d
+            a.B, a.ldb, a.b_stride = p.wgu.data_ptr(), d, 2 * F * d
+            if self.bf16:
+                a.C, a.ldc, a.c_stride, a.c_dtype = self.gu.data_ptr(), F, T * F, BF16
+                a.epilogue = EPI_SWIGLU
+                a.swiglu_block = p.swiglu_block
+            else:
+                a.C, a.ldc, a.c_stride, a.c_dtype = self.gu_full.data_ptr(), 2 * F, T * 2 * F, F32
+                a.epilogue = EPI_STORE
+            self._tables(a, gid, lrel, gid)
+        _lib.check(lib.armt_gemm(self._gemm(("gu",) + key, fill_gu), stream), "gate/up")
+        if not self.bf16:
+            _lib.check(lib.armt_swiglu(G, self.gu_full.data_ptr(), 2 * F, T * 2 * F, self.gu.data_ptr(), F, T * F,
+                                       F32, T, F, p.swiglu_block, stream), "swiglu")
+
+        def fill_down(a):
+            a.M, a.N, a.K, a.ab_dtype = T, d, F, p.ab
+            a.A, a.lda, a.a_stride = self.gu.data_ptr(), F, T * F
+            a.B, a.ldb, a.b_stride = p.wdown.data_ptr(), F, d * F
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.xs.data_ptr(), d, T * d, F32
+            a.epilogue = EPI_RESIDUAL
+            a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
+            if self.bf16:
+                a.C2, a.ldc2, a.c2_stride = self.xs_bf.data_ptr(), d, T * d
+            self._tables(a, gid, lrel, slots)
+        _lib.check(lib.armt_gemm(self._gemm(("down",) + key, fill_down), stream), "down-proj")
+
+    def update(self, slots, layers, state: MemoryState, stream: int) -> None:
+        """update_stack (armt/memory.py:155-180) from the memory rows of xs[slots]."""
+        p, cfg, lib = self.p, self.cfg, self.lib
+        T, d, M = p.T, cfg.d_model, cfg.num_mem_tokens
+        if M == 0:
+            return
+        lrel = [l - self.layer_base for l in layers]
+        gid = list(range(len(layers)))
+        src = self.xs_bf if self.bf16 else self.xs
+        esz = src.element_size()
+
+        def fill_kvb(a):
+            a.M, a.N, a.K, a.ab_dtype = M, p.n_kvb, d, p.ab
+            a.A, a.lda, a.a_stride = src.data_ptr() + cfg.segment_size * d * esz, d, T * d
+            a.B, a.ldb, a.b_stride = p.wkvb.data_ptr(), d, p.n_kvb * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, F32
+            a.epilogue = EPI_STORE
+            self._tables(a, slots, lrel, gid)
+        _lib.check(lib.armt_gemm(self._gemm(("kvb", tuple(slots), tuple(layers)), fill_kvb), stream), "kvb")
+        mem = self._members(slots, layers)
+        sh = state.shadow if self.bf16 else None
+        _lib.check(lib.armt_mem_fold(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off, p.b_off,
+                                     state.A.data_ptr(), state.z.data_ptr(), _ptr(sh), p.d_phi_pad, d, M,
+                                     cfg.d_mem, cfg.dpfp_nu, p.eps_assoc, self.fold_ws.data_ptr(), stream),
+                   "mem_fold")
+
+    def step(self, slots, layers, state: MemoryState, stream: int) -> None:
+        self.retrieve(slots, layers, state, stream)
+        self.forward(slots, layers, stream)
+        self.update(slots, layers, state, stream)
+
+    def unembed(self, slot: int, out: torch.Tensor, row0: int, stream: int) -> None:
+        """armt/layers.py:321-323: logits rows [row0, row0+seg) = xs[slot][:seg] @ U."""
+        p, cfg = self.p, self.cfg
+        d, V, seg = cfg.d_model, cfg.vocab_size, cfg.segment_size
+        src = self.xs_bf if self.bf16 else self.xs
+        odt = BF16 if out.dtype == torch.bfloat16 else F32
+
+        def fill(a):
+            a.M, a.N, a.K, a.ab_dtype = seg, V, d, p.ab
+            a.A, a.lda, a.a_stride = src.data_ptr(), d, p.T * d
+            a.B, a.ldb, a.b_stride = p.unemb.data_ptr(), d, V * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = out.data_ptr() + row0 * V * out.element_size(), V, seg * V, odt
+            a.epilogue = EPI_STORE
+            self._tables(a, [slot], [0], [0])
+        _lib.check(self.lib.armt_gemm(self._gemm(("lm", slot, out.data_ptr(), row0), fill), stream), "unembed")

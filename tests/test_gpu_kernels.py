@@ -1,0 +1,263 @@
+"""Kernel-level numerics on the B200 (``-m gpu``).
+
+Each kernel is called through the C-ABI (``armt_*``) and compared with a
+plain PyTorch fp32/fp64 reference of the same op on the same inputs:
+bf16-operand GEMMs against fp32 matmul of the bf16-rounded operands, f32
+SIMT GEMMs against fp64, attention against an explicit softmax, the memory
+fold against the oracle's in-order fold.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU hosts
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2506_05229_b200 import _lib  # noqa: E402
+from paper_2506_05229_b200._lib import BF16, F32  # noqa: E402
+
+DEV = torch.device("cuda")
+LIB = _lib.load()
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def rel(a, b):
+    a = a.double(); b = b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def gemm_args(G, M, N, K, A, B, C, ab, c_dtype, a_slots=None, b_idx=None, c_slots=None, **kw):
+    a = _lib.ArmtGemmArgs()
+    a.G, a.M, a.N, a.K, a.ab_dtype = G, M, N, K, ab
+    a.A, a.lda, a.a_stride = A.data_ptr(), K, M * K
+    a.B, a.ldb, a.b_stride = B.data_ptr(), K, N * K
+    a.C, a.ldc, a.c_stride, a.c_dtype = C.data_ptr(), kw.pop("ldc", N), kw.pop("c_stride", M * N), c_dtype
+    a.epilogue = kw.pop("epilogue", _lib.EPI_STORE)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    for g in range(G):
+        a.a_slot[g] = a_slots[g] if a_slots else g
+        a.b_index[g] = b_idx[g] if b_idx else g
+        a.c_slot[g] = c_slots[g] if c_slots else g
+    return a
+
+
+@pytest.mark.parametrize("M,N,K", [(1152, 2048, 2048), (80, 384, 128), (128, 256, 64), (200, 320, 96),
+                                   (16, 16, 8), (1152, 6144, 2048), (77, 1000, 520)])
+def test_tc_gemm_store_matches_fp32(M, N, K):
+    torch.manual_seed(0)
+    G, L = 3, 5
+    A = torch.randn(G + 1, M, K, device=DEV).bfloat16()
+    B = torch.randn(L, N, K, device=DEV).bfloat16()
+    C = torch.zeros(G, M, N, device=DEV)
+    slots, layers = [3, 0, 2], [4, 1, 2]
+    args = gemm_args(G, M, N, K, A, B, C, BF16, F32, slots, layers)
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+    for g in range(G):
+        want = A[slots[g]].float() @ B[layers[g]].float().T
+        assert rel(C[g], want) < 1e-5, (g, rel(C[g], want))
+
+
+def test_tc_gemm_bf16_out_and_residual():
+    torch.manual_seed(1)
+    G, M, N, K = 2, 300, 512, 256
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = torch.randn(G, N, K, device=DEV).bfloat16()
+    C = torch.zeros(G, M, N, device=DEV, dtype=torch.bfloat16)
+    _lib.check(LIB.armt_gemm(gemm_args(G, M, N, K, A, B, C, BF16, BF16), stream()), "gemm")
+    want = torch.einsum("gmk,gnk->gmn", A.float(), B.float())
+    assert rel(C, want) < 5e-3
+    R = torch.randn(G, M, N, device=DEV)
+    X = R.clone()
+    C2 = torch.zeros(G, M, N, device=DEV, dtype=torch.bfloat16)
+    args = gemm_args(G, M, N, K, A, B, X, BF16, F32, epilogue=_lib.EPI_RESIDUAL, R=X.data_ptr(), ldr=N,
+                     r_stride=M * N, C2=C2.data_ptr(), ldc2=N, c2_stride=M * N)
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+    assert rel(X, R + want) < 1e-5
+    assert rel(C2.float(), R + want) < 5e-3
+
+
+def test_tc_gemm_retrieve_epilogue():
+    torch.manual_seed(2)
+    G, M, N, K, eps = 2, 160, 256, 96, 0.5
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = torch.randn(G, N, K, device=DEV).bfloat16()
+    den = torch.randn(G, M, device=DEV)
+    den[:, :20] = 0.5  # exactly at eps: guarded (reads zero)
+    R = torch.randn(G, M, N, device=DEV)
+    X = R.clone()
+    args = gemm_args(G, M, N, K, A, B, X, BF16, F32, epilogue=_lib.EPI_RETRIEVE, R=X.data_ptr(), ldr=N,
+                     r_stride=M * N, den=den.data_ptr(), den_stride=M, eps=eps)
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+    acc = torch.einsum("gmk,gnk->gmn", A.float(), B.float())
+    guard = (den.abs() <= eps)[..., None]
+    want = R + torch.where(guard, torch.zeros_like(acc), acc / den[..., None])
+    assert rel(X, want) < 1e-5
+    assert torch.equal(X[:, :20], R[:, :20])
+
+
+@pytest.mark.parametrize("block", [32, 128])
+def test_tc_gemm_swiglu_epilogue(block):
+    torch.manual_seed(3)
+    G, M, K, F = 2, 200, 128, 512
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    gate = torch.randn(G, F, K, device=DEV) * 0.2
+    up = torch.randn(G, F, K, device=DEV) * 0.2
+    nt = F // block
+    B = torch.stack([gate.view(G, nt, block, K), up.view(G, nt, block, K)], 2).reshape(G, 2 * F, K).bfloat16()
+    C = torch.zeros(G, M, F, device=DEV, dtype=torch.bfloat16)
+    args = gemm_args(G, M, 2 * F, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_SWIGLU, swiglu_block=block,
+                     ldc=F, c_stride=M * F)
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+    gb = gate.bfloat16().float(); ub = up.bfloat16().float()
+    gv = torch.einsum("gmk,gfk->gmf", A.float(), gb)
+    uv = torch.einsum("gmk,gfk->gmf", A.float(), ub)
+    want = torch.nn.functional.silu(gv) * uv
+    assert rel(C.float(), want) < 5e-3
+
+
+@pytest.mark.parametrize("dh", [8, 32, 64, 128])
+def test_tc_gemm_rope_epilogue(dh):
+    torch.manual_seed(4)
+    H = 4
+    d = H * dh
+    G, M, K = 2, 144, 64
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = torch.randn(G, 3 * d, K, device=DEV).bfloat16()
+    C = torch.zeros(G, M, 3 * d, device=DEV, dtype=torch.bfloat16)
+    inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+    ang = np.arange(M)[:, None] * inv[None]
+    cos = torch.tensor(np.cos(ang), dtype=torch.float32, device=DEV)
+    sin = torch.tensor(np.sin(ang), dtype=torch.float32, device=DEV)
+    args = gemm_args(G, M, 3 * d, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_ROPE, rope_cos=cos.data_ptr(),
+                     rope_sin=sin.data_ptr(), head_dim=dh, rope_cols=2 * d)
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+    acc = torch.einsum("gmk,gnk->gmn", A.float(), B.float())
+    qk = acc[..., :2 * d].reshape(G, M, 2 * H, dh)
+    a, b = qk[..., :dh // 2], qk[..., dh // 2:]
+    c, s = cos[None, :, None], sin[None, :, None]
+    rot = torch.cat([a * c - b * s, b * c + a * s], -1).reshape(G, M, 2 * d)
+    want = torch.cat([rot, acc[..., 2 * d:]], -1)
+    assert rel(C.float(), want) < 5e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(80, 384, 128), (1152, 512, 2048), (6, 50, 16), (2, 8, 8)])
+def test_simt_gemm_matches_fp64(M, N, K):
+    torch.manual_seed(5)
+    G = 2
+    A = torch.randn(G, M, K, device=DEV)
+    B = torch.randn(G, N, K, device=DEV)
+    C = torch.zeros(G, M, N, device=DEV)
+    _lib.check(LIB.armt_gemm(gemm_args(G, M, N, K, A, B, C, F32, F32), stream()), "gemm")
+    want = torch.einsum("gmk,gnk->gmn", A.double(), B.double())
+    assert rel(C, want) < 1e-6
+
+
+def attention_ref(qkv, H, dh):
+    G, T, _ = qkv.shape
+    d = H * dh
+    q = qkv[..., :d].reshape(G, T, H, dh).transpose(1, 2).double()
+    k = qkv[..., d:2 * d].reshape(G, T, H, dh).transpose(1, 2).double()
+    v = qkv[..., 2 * d:].reshape(G, T, H, dh).transpose(1, 2).double()
+    s = q @ k.transpose(-1, -2) / math.sqrt(dh)
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool, device=qkv.device), 1)
+    s = s.masked_fill(mask, float("-inf"))
+    return (torch.softmax(s, -1) @ v).transpose(1, 2).reshape(G, T, d)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("T,H,dh", [(80, 4, 32), (1152, 4, 64), (144, 2, 128), (8, 2, 8), (200, 3, 16)])
+def test_attention_matches_reference(dtype, T, H, dh):
+    torch.manual_seed(6)
+    G = 2
+    d = H * dh
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    qkv = torch.randn(G, T, 3 * d, device=DEV).to(tdt)
+    ctx = torch.zeros(G, T, d, device=DEV, dtype=tdt)
+    _lib.check(LIB.armt_attention(G, qkv.data_ptr(), 3 * d, T * 3 * d, ctx.data_ptr(), d, T * d,
+                                  BF16 if dtype == "bf16" else F32, T, H, dh, 1.0 / math.sqrt(dh), stream()),
+               "attention")
+    want = attention_ref(qkv.float(), H, dh)
+    assert rel(ctx.float(), want) < (1e-2 if dtype == "bf16" else 1e-6)
+
+
+def test_dpfp_known_answers_on_device():
+    # pkg/tests/test_memory.py:25-33 pinned on the device feature map
+    from paper_2506_05229_b200.layers import dpfp
+    assert dpfp(torch.tensor([2.0], device=DEV), 3).cpu().tolist() == [0, 0, 4, 0, 0, 0]
+    assert dpfp(torch.tensor([-2.0], device=DEV), 3).cpu().tolist() == [0, 0, 0, 4, 0, 0]
+    assert dpfp(torch.tensor([1.0, -2.0], device=DEV), 1).cpu().tolist() == [0, 0, 0, 2]
+
+
+@pytest.mark.parametrize("d,M,d_mem,eps", [(128, 16, 16, 1.0), (2048, 128, 64, 1.0), (16, 2, 4, 1e-6),
+                                           (96, 5, 3, 0.1)])
+def test_fold_matches_oracle(d, M, d_mem, eps):
+    import armt_oracle as O
+    rng = np.random.default_rng(7)
+    nu = 3
+    dphi = 2 * nu * d_mem
+    G, L = 2, 3
+    layers = [2, 0]
+    A0 = (rng.standard_normal((L, d, dphi)) * 0.1).astype(np.float32)
+    z0 = np.abs(rng.standard_normal((L, dphi))).astype(np.float32)
+    n_kvb = ((d + d_mem + 1 + 15) // 16) * 16
+    kvb = np.zeros((G, M, n_kvb), np.float32)
+    kvb[:, :, :d] = rng.standard_normal((G, M, d))
+    kvb[:, :, d:d + d_mem] = rng.standard_normal((G, M, d_mem))
+    kvb[:, :, d + d_mem] = rng.standard_normal((G, M))
+    A = torch.tensor(A0, device=DEV)
+    z = torch.tensor(z0, device=DEV)
+    kv = torch.tensor(kvb, device=DEV)
+    ws = torch.empty(LIB.armt_fold_workspace_bytes(G, M, dphi) // 4 + 1, device=DEV)
+    mem = _lib.members([0, 1], layers)
+    _lib.check(LIB.armt_mem_fold(mem, kv.data_ptr(), n_kvb, M * n_kvb, 0, d, d + d_mem, A.data_ptr(),
+                                 z.data_ptr(), None, 0, d, M, d_mem, nu, eps, ws.data_ptr(), stream()), "fold")
+    for g, l in enumerate(layers):
+        Ar, zr = A0[l].astype(np.float64), z0[l].astype(np.float64)
+        # restate the fold inputs exactly as update_stack builds them
+        k = kvb[g, :, d:d + d_mem].astype(np.float64)
+        v = kvb[g, :, :d].astype(np.float64)
+        beta = O.sigmoid(kvb[g, :, d + d_mem].astype(np.float64))
+        phi = O.dpfp(k, nu)
+        for i in range(M):
+            p = phi[i]
+            zq = zr @ p
+            nrm = p @ p
+            vbar = np.zeros(d) if abs(zq) <= eps else (Ar @ p) / zq
+            gam = 0.0 if nrm <= eps else 1 - zq / nrm
+            Ar += np.outer(beta[i] * (v[i] - vbar), p)
+            zr += gam * p
+        assert rel(A[l].cpu(), torch.tensor(Ar)) < 1e-5
+        assert rel(z[l].cpu(), torch.tensor(zr)) < 1e-5
+    assert torch.equal(A[1].cpu(), torch.tensor(A0[1]))  # untouched layer
+
+
+def test_rmsnorm_matches_reference():
+    torch.manual_seed(8)
+    G, T, d, L = 3, 100, 256, 4
+    x = torch.randn(5, T, d, device=DEV)
+    gain = torch.rand(L, d, device=DEV) + 0.5
+    out = torch.empty(G, T, d, device=DEV)
+    mem = _lib.members([4, 1, 2], [3, 0, 0])
+    _lib.check(LIB.armt_rmsnorm(mem, x.data_ptr(), T * d, gain.data_ptr(), out.data_ptr(), F32, T * d, T, d,
+                                1e-6, stream()), "rmsnorm")
+    for g, (s, l) in enumerate([(4, 3), (1, 0), (2, 0)]):
+        xr = x[s].double()
+        want = xr / torch.sqrt((xr * xr).mean(-1, keepdim=True) + 1e-6) * gain[l].double()
+        assert rel(out[g], want) < 1e-6
+
+
+def test_kernel_counter_advances():
+    before = LIB.armt_kernel_count()
+    x = torch.zeros(16, device=DEV)
+    y = torch.zeros(16, device=DEV, dtype=torch.bfloat16)
+    _lib.check(LIB.armt_cast(x.data_ptr(), F32, y.data_ptr(), BF16, 16, stream()), "cast")
+    assert LIB.armt_kernel_count() == before + 1
