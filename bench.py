@@ -1,0 +1,366 @@
+"""Headline benchmark: tokens/s for one 131,072-token sequence through the
+LLaMA-3.2-1B-shaped ARMT (segment 1024, 128 memory tokens), bf16, on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--schedule diagonal|sequential]
+                    [--segments S] [--impl reference]
+
+One "step" = one full forward of the sequence (S+L-1 diagonal steps, every
+cell's retrieve/block/update plus the LM head for all tokens), replayed from
+a single CUDA graph with a fresh memory state; inputs (token ids, weights) are
+resident in HBM and far larger than L2 (3.3 GB of weights), so no flush is
+needed. ``e2e`` repeats the measurement through the public scoring API
+(``Session.nll``) with the token ids copied in from pinned host memory and
+the per-token NLL copied back every step.
+
+N > 1 (torchrun): layers are sharded contiguously across ranks (pipeline
+over the wavefront); the same 131,072 tokens are processed (strong scaling).
+``--impl reference`` times the CPU oracle port of the reference
+(oracle/armt_oracle.py) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+C2 = dict(n_layers=16, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024, num_mem_tokens=128,
+          d_mem=64, vocab_size=128256)
+N_TOKENS = 131072
+EPS_ASSOC = 100.0     # SURVEY Appendix B conditioning: finite over all 128 C2 segments (scripts/c2_horizon.py)
+METRIC = "tokens/sec for one 131k-token seq, LLaMA-1B ARMT seg1024, 1/2/4/8 B200"
+
+
+def cell_flops(cfg) -> float:
+    """Algorithmic FLOPs per (segment, layer) cell, SURVEY §8(d)."""
+    T, d, f, M, dm = cfg.tokens_per_segment, cfg.d_model, cfg.d_ff, cfg.num_mem_tokens, cfg.d_mem
+    dphi = cfg.d_phi
+    lin = 2 * T * (4 * d * d + 3 * d * f)
+    attn = 4 * d * T * (T + 1) / 2
+    retr = 2 * T * d * dm + 2 * T * dphi * d + 2 * T * dphi
+    upd = 2 * M * d * (dm + d + 1) + M * (4 * d * dphi + 6 * dphi)
+    return lin + attn + retr + upd
+
+
+def run_flops(cfg, n_segments: int) -> float:
+    return n_segments * cfg.n_layers * cell_flops(cfg) + 2 * n_segments * cfg.segment_size * cfg.d_model * cfg.vocab_size
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_weights(cfg):
+    """Reference initializer (armt/weights.py:98-138, seed 0), w_v_mem x 1/32."""
+    from dataclasses import replace
+    from paper_2506_05229_b200 import init_weights
+    w = init_weights(cfg, dtype=np.float32)
+    return replace(w, w_v_mem=w.w_v_mem * np.float32(1.0 / 32))
+
+
+def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: int = 16):
+    """Oracle (numpy/BLAS f32, all host threads) on full-width cells + one LM head,
+    extrapolated over the schedule: S*L cells + S heads."""
+    import armt_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        threads = os.cpu_count()
+    orc = O.Oracle(w, cfg, np.float32, eps_assoc=EPS_ASSOC)
+    rng = np.random.default_rng(0)
+    state = O.OracleState.fresh(cfg, np.float32)
+    x = orc.embed(rng.integers(0, cfg.vocab_size, cfg.segment_size))
+    x = orc.cell(state, 0, x)  # warm caches / BLAS pools
+    cells, t0 = 0, time.perf_counter()
+    while cells < max_cells and (cells < 2 or time.perf_counter() - t0 < budget_s):
+        x = orc.cell(state, cells % cfg.n_layers, x)
+        cells += 1
+    t_cell = (time.perf_counter() - t0) / cells
+    t1 = time.perf_counter()
+    orc.unembed(x)
+    t_lm = time.perf_counter() - t1
+    total = n_segments * cfg.n_layers * t_cell + n_segments * t_lm
+    return {"t_cell": t_cell, "t_lm": t_lm, "cells": cells, "total_s": total, "threads": threads,
+            "sample_s": cells * t_cell + t_lm}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_2506_05229_b200 import ModelConfig
+    cfg = ModelConfig(**C2, eps_assoc=EPS_ASSOC, seed=0)
+    n = N_TOKENS if args.segments is None else args.segments * cfg.segment_size
+    S = n // cfg.segment_size
+    w = make_weights(cfg)
+    rates, totals = [], []
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_rate(w, cfg, S, budget_s=4.0, max_cells=4)
+        if i >= args.warmup:
+            totals.append(r["total_s"])
+            rates.append(n / r["total_s"])
+    value = statistics.mean(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(totals),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded reference init, cli token convention)",
+            "config": {"workload": "C2: LLaMA-3.2-1B-shaped ARMT, seg 1024, 128 mem tokens, 131072 tokens",
+                       "schedule": "oracle cells (schedule-invariant per-cell cost)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                             "sample": f"per step: {r['cells']} full-width C2 cells (retrieve+block+fold) + 1 "
+                                       f"segment LM head in numpy/BLAS f32, extrapolated to {S}x{cfg.n_layers} "
+                                       f"cells + {S} heads"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- device arm
+def device_arm(args, rank, world):
+    import torch
+    from paper_2506_05229_b200 import ModelConfig
+    from paper_2506_05229_b200 import _lib
+    from paper_2506_05229_b200.engine import prepare_weights
+    from paper_2506_05229_b200.executors import Session
+
+    cfg = ModelConfig(**C2, eps_assoc=EPS_ASSOC, seed=0)
+    n = N_TOKENS if args.segments is None else args.segments * cfg.segment_size
+    S = -(-n // cfg.segment_size)
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    t_setup = time.time()
+    w = make_weights(cfg)
+    tokens = np.random.default_rng([0, n]).integers(0, cfg.vocab_size, n, dtype=np.int64)
+
+    if world > 1:
+        from paper_2506_05229_b200.sharded import ShardedSession
+        sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule)
+    else:
+        prep = prepare_weights(w, "bf16", dev)
+        sess = Session(prep, n, schedule=args.schedule)
+    sess._load_ids(torch.as_tensor(tokens).to(dev))
+
+    # roofline probe: events around every full-width gate/up GEMM, captured into the graph
+    probe_events = []
+    eng = sess.runner.engine
+    full_g = sess.plan.max_members
+
+    def probe(G, phase):
+        if G != full_g:
+            return
+        if phase == 0:
+            # external=True: event-record nodes that keep timing inside a CUDA graph
+            probe_events.append([torch.cuda.Event(enable_timing=True, external=True),
+                                 torch.cuda.Event(enable_timing=True, external=True)])
+            probe_events[-1][0].record()
+        else:
+            probe_events[-1][1].record()
+
+    sess.warm_eager()
+    eng.probe = probe
+    sess.capture()
+    eng.probe = None
+    setup_s = time.time() - t_setup
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        sess.forward()
+    torch.cuda.synchronize()
+    barrier()
+    probe_ms = []
+    step_ms = []
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sess.forward()
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            probe_ms.append(sum(a.elapsed_time(b) for a, b in probe_events))
+    barrier()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n / (ms_per_step / 1e3)
+
+    # end-to-end through the public scoring API: pinned H2D ids + D2H per-token NLL each step
+    host_ids = torch.as_tensor(tokens).pin_memory()
+    host_nll = torch.empty(n - 1, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        out = sess.nll(host_ids.to(dev, non_blocking=True))
+        host_nll.copy_(out, non_blocking=True) if out is not None else None
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = sess.nll(host_ids.to(dev, non_blocking=True))
+        if out is not None:
+            host_nll.copy_(out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = n / (e2e_total / args.steps / 1e3)
+    mean_nll = float(host_nll.mean()) if rank == world - 1 else None
+
+    peaks, peak_kind = load_peaks()
+    # dominant kernel: the grouped tcgen05 GEMM; probed launch = full-width gate/up (SwiGLU epilogue)
+    gu_flops = 2.0 * full_g * cfg.tokens_per_segment * (2 * sess.p.d_ff_pad) * cfg.d_model
+    n_probe = len(probe_events)
+    probe_avg_ms = statistics.mean(probe_ms) / max(n_probe, 1)
+    achieved = gu_flops / (probe_avg_ms / 1e3) / 1e12 if n_probe else None
+    peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
+    step_tflops = run_flops(cfg, S) / (ms_per_step / 1e3) / 1e12
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        r = cpu_oracle_rate(w, cfg, S)
+        cpu = {"value": n / r["total_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+               "sample": f"{r['cells']} full-width C2 cells (retrieve+block+fold) + 1 segment LM head, numpy/BLAS "
+                         f"f32 oracle ({r['sample_s']:.1f} s), extrapolated to {S}x{cfg.n_layers} cells + {S} heads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: reference seeded init (seed 0, w_v_mem/32, eps_assoc 100), cli token convention",
+        "config": {"workload": f"C2: LLaMA-3.2-1B-shaped ARMT (L16 d2048 H32 ff8192), seg 1024, 128 mem tokens, "
+                               f"{n} tokens", "schedule": args.schedule, "segments": S,
+                   "parallelism": f"layer-shard{world}" if world > 1 else "single",
+                   "l2": "inputs > L2 (3.3 GB bf16 weights, 33.6 GB logits); no flush",
+                   "timing": "CUDA events around one CUDA-graph replay of the whole forward, max over ranks",
+                   "whole_step_tflops": step_tflops,
+                   "whole_step_frac_of_sustained": step_tflops / peaks.get("bf16_tflops_sustained", peak),
+                   "setup_s": setup_s},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "kernel": f"tcgen05 grouped GEMM, gate/up (SwiGLU epilogue), G={full_g}, "
+                               f"{gu_flops / 1e12:.3f} TFLOP/launch, {n_probe} launches/step",
+                     "peak_kind": f"{peak_kind} bf16_tflops_sustained"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(n * 8),
+                "d2h_bytes_per_step": int((n - 1) * 4), "api": "Session.nll (pinned ids in, per-token NLL out)",
+                "mean_nll": mean_nll},
+        "gpu_launches": int(sess.kernels_per_forward * args.steps),
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--schedule", default="diagonal", choices=["diagonal", "sequential"])
+    ap.add_argument("--segments", type=int, default=None, help="override S (profiling runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    if world > 1:
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    try:
+        return device_arm(args, rank, world)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

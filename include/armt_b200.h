@@ -73,7 +73,7 @@ typedef struct {
   void* C2; long long ldc2, c2_stride;         /* RESIDUAL: optional bf16 copy, indexed by c_slot */
   const float* den; long long den_stride;      /* RETRIEVE: den[g*den_stride + m] */
   float eps;
-  const float* rope_cos; const float* rope_sin;  /* ROPE: (M rows, head_dim/2) tables */
+  const float* rope_cos; const float* rope_sin;  /* ROPE: (head_dim/2, M) tables, position-contiguous */
   int head_dim; int rope_cols;
   int swiglu_block;                     /* SWIGLU: cols [t*2b, t*2b+b) gate, [t*2b+b, (t+1)*2b) up */
   int a_slot[ARMT_MAX_MEMBERS];

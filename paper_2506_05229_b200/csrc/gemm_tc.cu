@@ -14,8 +14,10 @@
 //               stage; the last k-block commits "accumulator full".
 //   warp 2      TMEM allocator (2 accumulators x BN columns, double buffered
 //               so the epilogue of tile i overlaps the mainloop of tile i+1).
-//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 cols -> registers -> fused
-//               epilogue (residual / guarded retrieve / SwiGLU / RoPE) -> HBM.
+//   warps 4-11  epilogue, two warpgroups: warpgroup e drains TMEM accumulator e
+//               (every other tile), so each has two mainloop durations to run
+//               tcgen05.ld 32 lanes x 32 cols -> registers -> fused epilogue
+//               (residual / guarded retrieve / SwiGLU / RoPE) -> HBM.
 //
 // Tiles are ordered (member, n-block, m-block) with m fastest, so the CTAs in
 // flight share a few weight tiles (read once from HBM) and the member's
@@ -33,7 +35,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;  // 4 control warps + 2 epilogue warpgroups
 
 struct Params {
   int G, M, N, K;
@@ -187,14 +189,15 @@ __device__ __forceinline__ void load_row32_f32(const float* p, int cnt, bool vec
 
 // RoPE over one chunk of CH (>= DH, multiple of DH) columns held in registers.
 // Pairs (i, i + DH/2) inside each head; position = row within the segment.
+// cos/sin tables are (DH/2, ld) so a warp (32 consecutive rows) reads one line.
 template <int DH, int CH>
-__device__ __forceinline__ void rope_chunk(float (&x)[CH], const float* cos_row, const float* sin_row) {
+__device__ __forceinline__ void rope_chunk(float (&x)[CH], const float* cos_col, const float* sin_col, int ld) {
   constexpr int H2 = DH / 2;
 #pragma unroll
   for (int h = 0; h < CH / DH; ++h) {
 #pragma unroll
     for (int i = 0; i < H2; ++i) {
-      const float c = cos_row[i], s = sin_row[i];
+      const float c = cos_col[(long long)i * ld], s = sin_col[(long long)i * ld];
       const float a = x[h * DH + i], b = x[h * DH + i + H2];
       x[h * DH + i] = a * c - b * s;
       x[h * DH + i + H2] = b * c + a * s;
@@ -287,10 +290,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31
+    // ---------------- epilogue: warpgroup eg owns accumulator eg; TMEM lanes 32*(warp%4) .. +31
     const int ew = warp & 3;
-    int acc = 0; uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    const int eg = (warp - 4) >> 2;
+    const int acc = eg;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x + eg * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x) {
       const int g = tile / tiles_mn, r = tile - g * tiles_mn;
       const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
       const int row = mb * BM + ew * 32 + lane;
@@ -299,10 +304,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
 
       if constexpr (EPI == E_SWIGLU) {
         const int out_n0 = nb * (BN / 2);
-        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN / 2; c0 += 32) {
           float gte[32], up[32];
@@ -310,43 +315,57 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tmem_ld32(tbase + c0, gte);
           tmem_ld32(tbase + BN / 2 + c0, up);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) gte[j] = silu_ref(gte[j]) * up[j];
+          for (int j = 0; j < 32; ++j) gte[j] = gte[j] * __frcp_rn(1.f + __expf(-gte[j])) * up[j];
           if (live && out_n0 + c0 < p.N / 2) store_row32(p.C, ARMT_BF16, off, out_n0 + c0, p.N / 2, p.ldc, gte);
         }
       } else if constexpr (EPI == E_ROPE) {
+        // tables are (DH/2, M) column-major in position: lane = row reads consecutive words
+        const long long tr = live ? row : 0;
+        const float* cos_col = p.rope_cos + tr;
+        const float* sin_col = p.rope_sin + tr;
         constexpr int CH = DH > 32 ? DH : 32;
-        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
-        const float* cos_row = p.rope_cos + (long long)(live ? row : 0) * (DH / 2);
-        const float* sin_row = p.rope_sin + (long long)(live ? row : 0) * (DH / 2);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += CH) {
-          float x[CH];
-#pragma unroll
-          for (int q = 0; q < CH / 32; ++q) {
-            float t[32];
-            __syncwarp();
-            tmem_ld32(tbase + c0 + 32 * q, t);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) x[32 * q + j] = t[j];
-          }
           const int n0 = nb * BN + c0;
-          if (live && n0 < p.N) {
-            if (n0 < p.rope_cols) rope_chunk<DH, CH>(x, cos_row, sin_row);
+          const bool rot = n0 < p.rope_cols;
+          if constexpr (DH >= 64) {
+            // pairs (i, i + DH/2): rotate in 32-column sub-chunks to bound registers
+#pragma unroll 1
+            for (int q = 0; q < DH / 64; ++q) {
+              float x1[32], x2[32];
+              __syncwarp();
+              tmem_ld32(tbase + c0 + 32 * q, x1);
+              tmem_ld32(tbase + c0 + DH / 2 + 32 * q, x2);
+              if (live && n0 < p.N) {
+                if (rot) {
 #pragma unroll
-            for (int q = 0; q < CH / 32; ++q) {
-              float t[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) t[j] = x[32 * q + j];
-              if (n0 + 32 * q < p.N) store_row32(p.C, ARMT_BF16, off, n0 + 32 * q, p.N, p.ldc, t);
+                  for (int j = 0; j < 32; ++j) {
+                    const float cs = cos_col[(long long)(32 * q + j) * p.M], sn = sin_col[(long long)(32 * q + j) * p.M];
+                    const float a = x1[j], b = x2[j];
+                    x1[j] = a * cs - b * sn;
+                    x2[j] = b * cs + a * sn;
+                  }
+                }
+                store_row32(p.C, ARMT_BF16, off, n0 + 32 * q, p.N, p.ldc, x1);
+                store_row32(p.C, ARMT_BF16, off, n0 + DH / 2 + 32 * q, p.N, p.ldc, x2);
+              }
+            }
+          } else {
+            float x[32];
+            __syncwarp();
+            tmem_ld32(tbase + c0, x);
+            if (live && n0 < p.N) {
+              if (rot) rope_chunk<DH, 32>(x, cos_col, sin_col, p.M);
+              store_row32(p.C, ARMT_BF16, off, n0, p.N, p.ldc, x);
             }
           }
         }
       } else {
-        const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
-        float den = 1.f; bool guarded = false;
+        float rden = 1.f; bool guarded = false;
         if constexpr (EPI == E_RETRIEVE) {
-          if (live) den = p.den[(long long)g * p.den_stride + row];
+          const float den = live ? p.den[(long long)g * p.den_stride + row] : 1.f;
           guarded = fabsf(den) <= p.eps;
+          rden = 1.f / den;
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -362,7 +381,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                            ((p.ldr & 3) == 0) && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0), res);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if constexpr (EPI == E_RETRIEVE) v[j] = res[j] + (guarded ? 0.f : v[j] / den);
+              if constexpr (EPI == E_RETRIEVE) v[j] = res[j] + (guarded ? 0.f : v[j] * rden);
               else v[j] = res[j] + v[j];
             }
             store_row32(p.C, ARMT_F32, off, n0, p.N, p.ldc, v);
@@ -377,7 +396,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc ^= 1; if (acc == 0) acc_phase ^= 1;
+      acc_phase ^= 1;
     }
   }
 

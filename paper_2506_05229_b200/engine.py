@@ -75,8 +75,11 @@ class PreparedWeights:
     wqa: torch.Tensor
     wkvb: torch.Tensor
     unemb: torch.Tensor
-    rope_cos: torch.Tensor
+    rope_cos: torch.Tensor        # (T, d_head/2): stand-alone RoPE kernel (f32 mode)
     rope_sin: torch.Tensor
+    rope_cos_t: torch.Tensor      # (d_head/2, T): fused QKV epilogue (bf16 mode)
+    rope_sin_t: torch.Tensor
+    layer_base: int = 0
 
     @property
     def ab(self) -> int:
@@ -166,6 +169,8 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
         unemb=up("unembedding", False).t().contiguous().to(wdt),
         rope_cos=torch.as_tensor(np.cos(ang), dtype=torch.float32).to(dev).contiguous(),
         rope_sin=torch.as_tensor(np.sin(ang), dtype=torch.float32).to(dev).contiguous(),
+        rope_cos_t=torch.as_tensor(np.cos(ang).T, dtype=torch.float32).to(dev).contiguous(),
+        rope_sin_t=torch.as_tensor(np.sin(ang).T, dtype=torch.float32).to(dev).contiguous(),
     )
     prepared.layer_base = lo
     torch.cuda.synchronize(dev)
@@ -278,7 +283,7 @@ class Engine:
         nb = int(self.lib.armt_fold_workspace_bytes(G, cfg.num_mem_tokens, p.d_phi))
         self.fold_ws = torch.empty(max(nb, 16) // 4 + 1, device=dev)
         self._cache: dict = {}
-        self.launches_per_step = 12
+        self.probe = None   # optional callable(tag, phase) around the gate/up GEMM (bench roofline)
 
     # -- argument builders (memoised: graphs/eager replays reuse the structs) --
     def _gemm(self, key, fill):
@@ -372,7 +377,7 @@ class Engine:
             a.C, a.ldc, a.c_stride, a.c_dtype = self.qkv.data_ptr(), 3 * d, T * 3 * d, wout
             if self.bf16:
                 a.epilogue = EPI_ROPE
-                a.rope_cos, a.rope_sin = p.rope_cos.data_ptr(), p.rope_sin.data_ptr()
+                a.rope_cos, a.rope_sin = p.rope_cos_t.data_ptr(), p.rope_sin_t.data_ptr()
                 a.head_dim, a.rope_cols = p.d_head, 2 * d
             else:
                 a.epilogue = EPI_STORE
@@ -411,7 +416,11 @@ class Engine:
                 a.C, a.ldc, a.c_stride, a.c_dtype = self.gu_full.data_ptr(), 2 * F, T * 2 * F, F32
                 a.epilogue = EPI_STORE
             self._tables(a, gid, lrel, gid)
+        if self.probe is not None:
+            self.probe(G, 0)
         _lib.check(lib.armt_gemm(self._gemm(("gu",) + key, fill_gu), stream), "gate/up")
+        if self.probe is not None:
+            self.probe(G, 1)
         if not self.bf16:
             _lib.check(lib.armt_swiglu(G, self.gu_full.data_ptr(), 2 * F, T * 2 * F, self.gu.data_ptr(), F, T * F,
                                        F32, T, F, p.swiglu_block, stream), "swiglu")

@@ -243,15 +243,19 @@ class Runner:
         self._launch_all(state, stream, events)
         self.step_events = events
 
-    def capture(self, state: MemoryState) -> None:
+    def capture(self, state: MemoryState, reset_state: bool = False) -> None:
         """Record the whole run into one CUDA graph bound to ``state``'s
-        buffers (run eagerly once first so every kernel attribute is set)."""
+        buffers. With ``reset_state`` the graph starts from a fresh (zero)
+        memory, so every replay is an independent forward of the sequence."""
         self.graph_state = state
         side = torch.cuda.Stream(device=self.p.device)
         side.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, stream=side):
+                if reset_state:
+                    state.A.zero_()
+                    state.z.zero_()
                 state.sync_shadow(self.p)
                 self._launch_all(state, side.cuda_stream)
         torch.cuda.current_stream().wait_stream(side)
@@ -347,3 +351,92 @@ def run_diagonal(weights, config: ModelConfig, tokens, *, dtype: str = "bf16", t
         raise InputError(f"threads must be a positive int, got {threads!r}")
     return _run("diagonal", weights, config, tokens, dtype, state, shuffle_seed, device, graph,
                 return_numpy, timed)
+
+
+# =========================================================================
+# Session: the reusable user-facing call for repeated sequences
+# =========================================================================
+
+class Session:
+    """A compiled forward for sequences of a fixed length.
+
+    Holds prepared weights, the activation workspace, its own memory state
+    and ONE CUDA graph of the whole schedule (every step's launches). Each
+    call copies the token ids in, replays the graph from a fresh memory
+    state and returns device logits, or — for scoring, the end-to-end path —
+    the next-token negative log-likelihood (mean, per token).
+    """
+
+    def __init__(self, prepared: PreparedWeights, n_tokens: int, schedule: str = "diagonal",
+                 graph: bool = True, shuffle_seed: int | None = None):
+        cfg = prepared.config
+        self.p, self.cfg, self.n = prepared, cfg, int(n_tokens)
+        S = -(-self.n // cfg.segment_size)
+        if schedule == "diagonal":
+            plan = diagonal_plan(S, cfg.n_layers, shuffle_seed)
+        elif schedule == "sequential":
+            plan = sequential_plan(S, cfg.n_layers)
+        else:
+            raise InputError(f"unknown schedule {schedule!r}")
+        self.plan = plan
+        self.runner = Runner(prepared, plan)
+        self.state = MemoryState.fresh(cfg, prepared.device)
+        self.nll_rows = torch.empty(max(self.n - 1, 1), device=prepared.device)
+        self.use_graph = graph
+        self.kernels_per_forward = None
+
+    def _load_ids(self, tokens) -> None:
+        ids = self.runner.ids
+        if isinstance(tokens, torch.Tensor):
+            if tokens.numel() != self.n:
+                raise InputError(f"session compiled for {self.n} tokens, got {tokens.numel()}")
+            ids[:self.n].copy_(tokens.reshape(-1), non_blocking=True)
+        else:
+            segs, n = segment_input(tokens, self.cfg)
+            if n != self.n:
+                raise InputError(f"session compiled for {self.n} tokens, got {n}")
+            ids.copy_(torch.as_tensor(np.concatenate(segs)))
+        if self.n < ids.numel():
+            ids[self.n:].zero_()
+
+    def warm_eager(self) -> None:
+        """One eager pass: sets kernel attributes and counts the launches."""
+        from . import _lib
+        self.state.A.zero_(); self.state.z.zero_()
+        before = _lib.kernel_count()
+        self.runner.run(self.state)
+        torch.cuda.synchronize()
+        self.kernels_per_forward = _lib.kernel_count() - before
+
+    def capture(self) -> None:
+        self.runner.capture(self.state, reset_state=True)
+
+    def warm(self) -> None:
+        self.warm_eager()
+        if self.use_graph:
+            self.capture()
+
+    def forward(self, tokens=None) -> torch.Tensor:
+        if tokens is not None:
+            self._load_ids(tokens)
+        if self.use_graph:
+            if self.runner.graph is None:
+                self.warm()
+            self.runner.replay()
+        else:
+            self.state.A.zero_(); self.state.z.zero_()
+            self.runner.run(self.state)
+        return self.runner.logits[:self.n]
+
+    def nll(self, tokens=None, targets: torch.Tensor | None = None) -> torch.Tensor:
+        """Per-token next-token NLL (device, n-1 values); targets default to
+        the input ids shifted by one."""
+        from . import _lib
+        logits = self.forward(tokens)
+        if targets is None:
+            targets = self.runner.ids[1:self.n]
+        odt = _lib.BF16 if logits.dtype == torch.bfloat16 else _lib.F32
+        _lib.check(_lib.load().armt_logits_nll(logits.data_ptr(), odt, self.cfg.vocab_size, targets.data_ptr(),
+                                               self.nll_rows.data_ptr(), self.n - 1, self.cfg.vocab_size,
+                                               torch.cuda.current_stream().cuda_stream), "nll")
+        return self.nll_rows[:self.n - 1]

@@ -1,0 +1,127 @@
+"""Per-kernel timing of the C2 hot ops at a given member count (CUDA events),
+for ncu captures and kernel iteration.
+
+    python scripts/kernel_bench.py [--G 16] [--ops gu,down,qkv,o,attn,fold,lm] [--iters 20]
+
+Prints one JSON line per op: avg us/launch, achieved TFLOP/s (GEMMs/attention)
+or GB/s (fold), fraction of MEASURED_PEAKS.
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2506_05229_b200 import _lib  # noqa: E402
+from paper_2506_05229_b200._lib import BF16, F32  # noqa: E402
+
+LIB = _lib.load()
+T, d, F, H, dh, M, dm, V, L = 1152, 2048, 8192, 32, 64, 128, 64, 128256, 16
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {"bf16_tflops_sustained": 1400.0, "bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+
+
+def timeit(fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / iters  # us
+
+
+def gemm(G, Mr, N, K, epi=_lib.EPI_STORE, c_dtype=BF16, **kw):
+    A = torch.randn(G, Mr, K, device="cuda").bfloat16()
+    B = (torch.randn(L if G <= L else G, N, K, device="cuda") * 0.02).bfloat16()
+    ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
+    C = torch.zeros(G, Mr, ncol, device="cuda", dtype=torch.float32 if c_dtype == F32 else torch.bfloat16)
+    a = _lib.ArmtGemmArgs()
+    a.G, a.M, a.N, a.K, a.ab_dtype = G, Mr, N, K, BF16
+    a.A, a.lda, a.a_stride = A.data_ptr(), K, Mr * K
+    a.B, a.ldb, a.b_stride = B.data_ptr(), K, N * K
+    a.C, a.ldc, a.c_stride, a.c_dtype = C.data_ptr(), ncol, Mr * ncol, c_dtype
+    a.epilogue = epi
+    keep = [A, B, C]
+    if epi in (_lib.EPI_RESIDUAL,):
+        a.R, a.ldr, a.r_stride = C.data_ptr(), ncol, Mr * ncol
+    if epi == _lib.EPI_SWIGLU:
+        a.swiglu_block = 128
+    if epi == _lib.EPI_ROPE:
+        inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+        ang = np.arange(Mr)[:, None] * inv[None]
+        cs = torch.tensor(np.cos(ang).T.copy(), dtype=torch.float32, device="cuda")
+        sn = torch.tensor(np.sin(ang).T.copy(), dtype=torch.float32, device="cuda")
+        keep += [cs, sn]
+        a.rope_cos, a.rope_sin, a.head_dim, a.rope_cols = cs.data_ptr(), sn.data_ptr(), dh, 2 * d
+    for g in range(G):
+        a.a_slot[g] = g
+        a.b_index[g] = g % B.shape[0]
+        a.c_slot[g] = g
+    s = torch.cuda.current_stream().cuda_stream
+    return (lambda: _lib.check(LIB.armt_gemm(a, s), "gemm")), 2.0 * G * Mr * N * K, keep
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--G", type=int, default=16)
+    ap.add_argument("--ops", default="gu,down,qkv,o,kvb,num,attn,fold,lm")
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    G = args.G
+    pk = peaks()
+    for op in args.ops.split(","):
+        if op in ("gu", "down", "qkv", "o", "kvb", "num", "lm"):
+            spec = {"gu": (G, T, 2 * F, d, _lib.EPI_SWIGLU, BF16), "down": (G, T, d, F, _lib.EPI_RESIDUAL, F32),
+                    "qkv": (G, T, 3 * d, d, _lib.EPI_ROPE, BF16), "o": (G, T, d, d, _lib.EPI_RESIDUAL, F32),
+                    "kvb": (G, M, 2128, d, _lib.EPI_STORE, F32), "num": (G, T, d, 384, _lib.EPI_STORE, F32),
+                    "lm": (1, 1024, V, d, _lib.EPI_STORE, BF16)}[op]
+            fn, flops, keep = gemm(*spec)
+            us = timeit(fn, args.iters)
+            tf = flops / us / 1e6
+            print(json.dumps({"op": op, "G": spec[0], "us": us, "tflops": tf,
+                              "frac_sustained": tf / pk["bf16_tflops_sustained"]}), flush=True)
+        elif op == "attn":
+            qkv = torch.randn(G, T, 3 * d, device="cuda").bfloat16()
+            ctx = torch.empty(G, T, d, device="cuda", dtype=torch.bfloat16)
+            s = torch.cuda.current_stream().cuda_stream
+            fn = lambda: _lib.check(LIB.armt_attention(G, qkv.data_ptr(), 3 * d, T * 3 * d, ctx.data_ptr(), d, T * d,
+                                                       BF16, T, H, dh, 1 / math.sqrt(dh), s), "attn")
+            us = timeit(fn, args.iters)
+            flops = G * 4 * d * T * (T + 1) / 2
+            print(json.dumps({"op": "attn", "G": G, "us": us, "tflops": flops / us / 1e6,
+                              "frac_sustained": flops / us / 1e6 / pk["bf16_tflops_sustained"]}), flush=True)
+        elif op == "fold":
+            dphi = 6 * dm
+            A = torch.randn(L, d, dphi, device="cuda") * 0.01
+            z = torch.rand(L, dphi, device="cuda") * 10
+            nk = 2128
+            kvb = torch.randn(G, M, nk, device="cuda")
+            ws = torch.empty(LIB.armt_fold_workspace_bytes(G, M, dphi) // 4 + 1, device="cuda")
+            mem = _lib.members(list(range(G)), list(range(G)))
+            s = torch.cuda.current_stream().cuda_stream
+            fn = lambda: _lib.check(LIB.armt_mem_fold(mem, kvb.data_ptr(), nk, M * nk, 0, d, d + dm, A.data_ptr(),
+                                                      z.data_ptr(), None, 0, d, M, dm, 3, 10.0, ws.data_ptr(), s), "fold")
+            us = timeit(fn, args.iters)
+            byts = G * (2 * d * dphi * 4 + M * nk * 4)
+            fl = G * M * d * dphi * 4
+            print(json.dumps({"op": "fold", "G": G, "us": us, "GBps": byts / us / 1e3, "fp32_tflops": fl / us / 1e6,
+                              "frac_hbm": byts / us / 1e3 / pk["hbm_gbs"]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

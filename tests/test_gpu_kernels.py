@@ -137,8 +137,9 @@ def test_tc_gemm_rope_epilogue(dh):
     ang = np.arange(M)[:, None] * inv[None]
     cos = torch.tensor(np.cos(ang), dtype=torch.float32, device=DEV)
     sin = torch.tensor(np.sin(ang), dtype=torch.float32, device=DEV)
-    args = gemm_args(G, M, 3 * d, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_ROPE, rope_cos=cos.data_ptr(),
-                     rope_sin=sin.data_ptr(), head_dim=dh, rope_cols=2 * d)
+    cos_t, sin_t = cos.t().contiguous(), sin.t().contiguous()
+    args = gemm_args(G, M, 3 * d, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_ROPE, rope_cos=cos_t.data_ptr(),
+                     rope_sin=sin_t.data_ptr(), head_dim=dh, rope_cols=2 * d)
     _lib.check(LIB.armt_gemm(args, stream()), "gemm")
     acc = torch.einsum("gmk,gnk->gmn", A.float(), B.float())
     qk = acc[..., :2 * d].reshape(G, M, 2 * H, dh)
