@@ -211,48 +211,52 @@ __global__ void __launch_bounds__(128) attn_bf16_kernel(const __nv_bfloat16* __r
         mma16816(s[nt + 1], qf[kk], b[2], b[3]);
       }
     }
-    // scale, mask (causal + keys beyond T), online softmax
+    // online softmax: running max on raw scores; p = exp2(s*scale_log2 - m*scale_log2)
+    // (one FFMA + EX2 per element; masked scores are -inf and exp2(-inf) = 0).
     const int k0 = kt * BKV;
-    const bool need_mask = (k0 + BKV - 1 > q0 + warp * 16) || (k0 + BKV > T);
+    if ((k0 + BKV - 1 > q0 + warp * 16) || (k0 + BKV > T)) {  // diagonal / tail tile only
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = qr0 + (e >> 1) * 8;
+          const int key = k0 + nt * 8 + 2 * tig + (e & 1);
+          if (key > row || key >= T) s[nt][e] = -INFINITY;
+        }
+    }
     float mx[2] = {mrow[0], mrow[1]};
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int row = qr0 + (e >> 1) * 8;
-        const int key = k0 + nt * 8 + 2 * tig + (e & 1);
-        float v = s[nt][e] * scale_log2;
-        if (need_mask && (key > row || key >= T)) v = -INFINITY;
-        s[nt][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
+      mx[0] = fmaxf(mx[0], fmaxf(s[nt][0], s[nt][1]));
+      mx[1] = fmaxf(mx[1], fmaxf(s[nt][2], s[nt][3]));
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
       mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
     }
-    float corr[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mx[r]);
-      mrow[r] = mx[r];
-      lrow[r] *= corr[r];
-    }
+    // every processed tile holds at least one unmasked key per row, so mx is finite
+    const float corr0 = exp2f((mrow[0] - mx[0]) * scale_log2);
+    const float corr1 = exp2f((mrow[1] - mx[1]) * scale_log2);
+    mrow[0] = mx[0];
+    mrow[1] = mx[1];
+    const float nm0 = -mx[0] * scale_log2, nm1 = -mx[1] * scale_log2;
+    float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = e >> 1;
-        const float p = (s[nt][e] == -INFINITY) ? 0.f : exp2f(s[nt][e] - mx[r]);
-        s[nt][e] = p;
-        lrow[r] += p;
-      }
+      s[nt][0] = exp2f(fmaf(s[nt][0], scale_log2, nm0));
+      s[nt][1] = exp2f(fmaf(s[nt][1], scale_log2, nm0));
+      s[nt][2] = exp2f(fmaf(s[nt][2], scale_log2, nm1));
+      s[nt][3] = exp2f(fmaf(s[nt][3], scale_log2, nm1));
+      ls0 += s[nt][0] + s[nt][1];
+      ls1 += s[nt][2] + s[nt][3];
     }
+    lrow[0] = lrow[0] * corr0 + ls0;
+    lrow[1] = lrow[1] * corr1 + ls1;
 #pragma unroll
     for (int i = 0; i < DH / 8; ++i) {
-      o[i][0] *= corr[0]; o[i][1] *= corr[0];
-      o[i][2] *= corr[1]; o[i][3] *= corr[1];
+      o[i][0] *= corr0; o[i][1] *= corr0;
+      o[i][2] *= corr1; o[i][3] *= corr1;
     }
     // O += P V
 #pragma unroll

@@ -151,34 +151,49 @@ __global__ void cast_kernel(const S* __restrict__ src, D* __restrict__ dst, long
 }
 
 // ------------------------------------------------------------------ NLL
+// One CTA per row: single pass of online log-sum-exp over 16-byte vectors.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
+}
+
 template <typename T>
-__global__ void nll_kernel(const T* __restrict__ logits, long long ld, const long long* __restrict__ tgt,
-                           float* __restrict__ nll, int vocab) {
+__global__ void __launch_bounds__(256) nll_kernel(const T* __restrict__ logits, long long ld,
+                                                  const long long* __restrict__ tgt, float* __restrict__ nll,
+                                                  int vocab) {
+  constexpr int VEC = 16 / sizeof(T);
   const long long row = blockIdx.x;
   const T* r = logits + row * ld;
-  __shared__ float red[32];
-  float m = -INFINITY;
-  for (int c = threadIdx.x; c < vocab; c += blockDim.x) m = fmaxf(m, to_f32(r[c]));
-  m = warp_max(m);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
-    v = warp_max(v);
-    if (threadIdx.x == 0) red[0] = v;
+  float m = -INFINITY, s = 0.f;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(r) & 15) == 0);
+  const int nvec = aligned ? vocab / VEC : 0;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    uint4 raw;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w) : "l"(reinterpret_cast<const uint4*>(r) + v));
+    const T* e = reinterpret_cast<const T*>(&raw);
+    float bm = to_f32(e[0]);
+#pragma unroll
+    for (int j = 1; j < VEC; ++j) bm = fmaxf(bm, to_f32(e[j]));
+    float bs = 0.f;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) bs += __expf(to_f32(e[j]) - bm);
+    lse_merge(m, s, bm, bs);
   }
+  for (int c = nvec * VEC + threadIdx.x; c < vocab; c += blockDim.x) lse_merge(m, s, to_f32(r[c]), 1.f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_merge(m, s, m2, s2);
+  }
+  __shared__ float sm_m[8], sm_s[8];
+  if ((threadIdx.x & 31) == 0) { sm_m[threadIdx.x >> 5] = m; sm_s[threadIdx.x >> 5] = s; }
   __syncthreads();
-  m = red[0];
-  __syncthreads();
-  float s = 0.f;
-  for (int c = threadIdx.x; c < vocab; c += blockDim.x) s += __expf(to_f32(r[c]) - m);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) nll[row] = m + logf(v) - to_f32(r[tgt[row]]);
+  if (threadIdx.x == 0) {
+    float M = sm_m[0], S = sm_s[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) lse_merge(M, S, sm_m[w], sm_s[w]);
+    nll[row] = M + logf(S) - to_f32(r[tgt[row]]);
   }
 }
 
@@ -283,10 +298,10 @@ int armt_logits_nll(const void* logits, int dtype, long long ld, const long long
                     long long rows, int vocab, void* stream) {
   if (rows <= 0) return ARMT_OK;
   if (dtype == ARMT_BF16)
-    nll_kernel<<<(unsigned)rows, 512, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(logits), ld,
+    nll_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(logits), ld,
                                                               targets, nll, vocab);
   else
-    nll_kernel<<<(unsigned)rows, 512, 0, as_stream(stream)>>>(reinterpret_cast<const float*>(logits), ld, targets,
+    nll_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(reinterpret_cast<const float*>(logits), ld, targets,
                                                               nll, vocab);
   ARMT_CHECK_LAUNCH("nll");
   return ARMT_OK;

@@ -262,3 +262,17 @@ def test_kernel_counter_advances():
     y = torch.zeros(16, device=DEV, dtype=torch.bfloat16)
     _lib.check(LIB.armt_cast(x.data_ptr(), F32, y.data_ptr(), BF16, 16, stream()), "cast")
     assert LIB.armt_kernel_count() == before + 1
+
+
+@pytest.mark.parametrize("dtype,V", [("bf16", 128256), ("f32", 1000), ("bf16", 50)])
+def test_logits_nll_matches_log_softmax(dtype, V):
+    torch.manual_seed(9)
+    rows = 37
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    logits = (torch.randn(rows, V, device=DEV) * 4).to(tdt)
+    tgt = torch.randint(0, V, (rows,), device=DEV)
+    out = torch.empty(rows, device=DEV)
+    _lib.check(LIB.armt_logits_nll(logits.data_ptr(), BF16 if dtype == "bf16" else F32, V, tgt.data_ptr(),
+                                   out.data_ptr(), rows, V, stream()), "nll")
+    want = -torch.log_softmax(logits.double(), -1).gather(1, tgt[:, None])[:, 0]
+    assert rel(out, want) < 1e-5

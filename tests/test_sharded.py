@@ -1,0 +1,128 @@
+"""Layer-sharded pipeline: plan invariants and a world-size-2 gloo run on CPU.
+
+The CPU run drives the product's ``run_stage``/``stage_plan`` with an oracle
+backend (test-only) and torch.distributed gloo point-to-point, and must equal
+the unsharded oracle diagonal run bitwise (every cell is computed by the same
+arithmetic; only the placement and the hand-offs change).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import C1
+from paper_2506_05229_b200.config import ModelConfig
+from paper_2506_05229_b200.scheduler import diagonal_members
+from paper_2506_05229_b200.sharded import TorchP2P, layer_blocks, run_stage, stage_plan
+
+
+@pytest.mark.parametrize("S,L,P", [(8, 16, 2), (128, 16, 8), (3, 5, 4), (1, 4, 4), (10, 7, 3), (5, 2, 1)])
+def test_stage_plans_cover_the_wavefront(S, L, P):
+    plans = [stage_plan(S, L, r, P) for r in range(P)]
+    assert [p.layers for p in plans] == layer_blocks(L, P)
+    for i in range(S + L - 1):
+        union = [n for p in plans for n in p.steps[i].nodes]
+        assert union == diagonal_members(i, S, L)
+    for r, p in enumerate(plans):
+        for i, st in enumerate(p.steps):
+            if st.recv is not None:  # matched by rank r-1's send one step earlier
+                assert plans[r - 1].steps[i - 1].send == (st.recv[0], plans[r - 1].steps[i - 1].send[1])
+            if st.exits:
+                assert r == P - 1
+            if st.enter:
+                assert r == 0
+            # no two in-flight segments share a slot on this rank
+            inflight = {n.segment for n in st.nodes}
+            slots = [s % p.n_slots for s in inflight]
+            assert len(set(slots)) == len(slots)
+            for n, slot in zip(st.nodes, st.slots):
+                assert slot == n.segment % p.n_slots
+
+
+class OracleBackend:
+    """Test-only backend: oracle cells on CPU tensors (gloo moves them)."""
+
+    def __init__(self, orc, layers, n_slots, tokens):
+        import armt_oracle as O
+        self.orc = orc
+        self.state = O.OracleState.fresh(orc.cfg, np.float64)
+        self.slots = [torch.zeros(orc.T, orc.cfg.d_model, dtype=torch.float64) for _ in range(n_slots)]
+        self.segs, self.n = O.segment_input(tokens, orc.cfg)
+        self.rows = {}
+
+    def slot_tensor(self, slot):
+        return self.slots[slot]
+
+    def after_recv(self, slot):
+        pass
+
+    def embed(self, s, slot):
+        self.slots[slot].copy_(torch.from_numpy(self.orc.embed(self.segs[s])))
+
+    def step(self, slots, layers):
+        for slot, l in zip(slots, layers):
+            y = self.orc.cell(self.state, l, self.slots[slot].numpy().copy())
+            self.slots[slot].copy_(torch.from_numpy(y))
+
+    def unembed(self, s, slot):
+        self.rows[s] = self.orc.unembed(self.slots[slot].numpy())
+
+
+def _worker(rank, world, port, tokens, out_q):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle"))
+    import armt_oracle as O
+    from fixtures import conditioned_weights
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = ModelConfig(**C1, eps_assoc=1.0)
+    orc = O.Oracle(conditioned_weights(cfg), cfg, np.float64)
+    S = len(tokens) // cfg.segment_size
+    plan = stage_plan(S, cfg.n_layers, rank, world)
+    be = OracleBackend(orc, plan.layers, plan.n_slots, tokens)
+    run_stage(plan, be, TorchP2P(dist))
+    own = [l for l in plan.layers]
+    out_q.put((rank, be.rows, be.state.A[own].copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_two_rank_gloo_pipeline_equals_unsharded_oracle():
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle"))
+    import armt_oracle as O
+    from fixtures import cli_tokens, conditioned_weights
+    cfg = ModelConfig(**C1, eps_assoc=1.0)
+    tokens = cli_tokens(cfg, 5 * cfg.segment_size, seed=11)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, tokens, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict()
+    for _ in range(2):
+        r, rows, A = q.get(timeout=300)
+        results[r] = (rows, A)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want, wstate, _ = O.Oracle(conditioned_weights(cfg), cfg, np.float64).run_diagonal(tokens)
+    rows = results[1][0]
+    got = np.concatenate([rows[s] for s in range(5)])
+    assert np.array_equal(got, want)
+    assert np.array_equal(results[0][1], wstate.A[0:1])
+    assert np.array_equal(results[1][1], wstate.A[1:2])
