@@ -71,6 +71,7 @@ typedef struct {
   int epilogue;                         /* ArmtEpilogue */
   const float* R; long long ldr, r_stride;     /* RESIDUAL/RETRIEVE input, indexed by c_slot */
   void* C2; long long ldc2, c2_stride;         /* RESIDUAL: optional bf16 copy, indexed by c_slot */
+  int c2_split;                         /* >0: C2 gets [hi | lo | hi] bf16 split of C at cols n, n+s, n+2s */
   const float* den; long long den_stride;      /* RETRIEVE: den[g*den_stride + m] */
   float eps;
   const float* rope_cos; const float* rope_sin;  /* ROPE: (head_dim/2, M) tables, position-contiguous */
@@ -132,6 +133,19 @@ int armt_mem_fold(const ArmtMembers* mem, const float* kvb, long long ld_kvb,
                   void* A_shadow, long long ld_shadow, int d, int n_mem, int d_mem, int nu,
                   float eps, void* ws, void* stream);
 long long armt_fold_workspace_bytes(int G, int n_mem, int d_phi);
+
+/* Tensor-core form of the same fold for the bf16 path (chunked delta rule:
+ * U = L^{-1} R with L = I + diag(c) tril(Phi Phi^T, -1), A += U^T Phi; two grouped
+ * tcgen05 GEMMs on bf16x3-split operands). `memop` (L, armt_memop_rows(d, M), 3*P) bf16,
+ * P = d_phi rounded up to 8, holds per layer the [hi|lo|hi] split of A (rows 0..d-1),
+ * of z (row d) and of the member's phi (rows d+8..); retrieval reads its hi part.
+ * ws: armt_fold_tc_workspace_bytes(G, M, d, d_phi) bytes, zero-initialised once. */
+int armt_mem_fold_tc(const ArmtMembers* mem, const float* kvb, long long ld_kvb,
+                     long long kvb_stride, int v_off, int k_off, int b_off, float* A, float* z,
+                     void* memop, int d, int n_mem, int d_mem, int nu, float eps, void* ws,
+                     void* stream);
+long long armt_fold_tc_workspace_bytes(int G, int n_mem, int d, int d_phi);
+long long armt_memop_rows(int d, int n_mem);
 
 /* Elementwise copy/cast between f32 and bf16 buffers (n elements). */
 int armt_cast(const void* src, int src_dtype, void* dst, int dst_dtype, long long n, void* stream);

@@ -24,7 +24,8 @@ EPI_STORE, EPI_RESIDUAL, EPI_RETRIEVE, EPI_SWIGLU, EPI_ROPE = 0, 1, 2, 3, 4
 EXPORTS = ("armt_gemm", "armt_embed", "armt_rmsnorm", "armt_dpfp_den", "armt_attention",
            "armt_rope", "armt_swiglu", "armt_mem_fold", "armt_fold_workspace_bytes", "armt_cast",
            "armt_logits_nll", "armt_last_error", "armt_version", "armt_num_sms",
-           "armt_kernel_count", "armt_abi_sizeof")
+           "armt_kernel_count", "armt_abi_sizeof", "armt_mem_fold_tc", "armt_fold_tc_workspace_bytes",
+           "armt_memop_rows")
 
 _I = ctypes.c_int
 _LL = ctypes.c_longlong
@@ -46,6 +47,7 @@ class ArmtGemmArgs(ctypes.Structure):
         ("epilogue", _I),
         ("R", _P), ("ldr", _LL), ("r_stride", _LL),
         ("C2", _P), ("ldc2", _LL), ("c2_stride", _LL),
+        ("c2_split", _I),
         ("den", _P), ("den_stride", _LL),
         ("eps", _F),
         ("rope_cos", _P), ("rope_sin", _P),
@@ -81,6 +83,10 @@ def load(path: str = LIB_PATH):
         "armt_mem_fold": (_I, [ctypes.POINTER(ArmtMembers), _P, _LL, _LL, _I, _I, _I, _P, _P, _P, _LL,
                                _I, _I, _I, _I, _F, _P, _P]),
         "armt_fold_workspace_bytes": (_LL, [_I, _I, _I]),
+        "armt_mem_fold_tc": (_I, [ctypes.POINTER(ArmtMembers), _P, _LL, _LL, _I, _I, _I, _P, _P, _P,
+                                  _I, _I, _I, _I, _F, _P, _P]),
+        "armt_fold_tc_workspace_bytes": (_LL, [_I, _I, _I, _I]),
+        "armt_memop_rows": (_LL, [_I, _I]),
         "armt_cast": (_I, [_P, _I, _P, _I, _LL, _P]),
         "armt_logits_nll": (_I, [_P, _I, _LL, _P, _P, _LL, _I, _P]),
         "armt_last_error": (ctypes.c_char_p, []),

@@ -43,7 +43,7 @@ struct Params {
   int c_dtype;
   void* C; long long ldc, c_stride;
   const float* R; long long ldr, r_stride;
-  __nv_bfloat16* C2; long long ldc2, c2_stride;
+  __nv_bfloat16* C2; long long ldc2, c2_stride; int c2_split;
   const float* den; long long den_stride;
   float eps;
   const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
@@ -385,9 +385,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               else v[j] = res[j] + v[j];
             }
             store_row32(p.C, ARMT_F32, off, n0, p.N, p.ldc, v);
-            if (EPI == E_RESIDUAL && p.C2 != nullptr)
-              store_row32(p.C2, ARMT_BF16, (long long)c_slot * p.c2_stride + (long long)row * p.ldc2,
-                          n0, p.N, p.ldc2, v);
+            if (EPI == E_RESIDUAL && p.C2 != nullptr) {
+              const long long off2 = (long long)c_slot * p.c2_stride + (long long)row * p.ldc2;
+              if (p.c2_split > 0) {
+                // bf16x3 operand layout [hi | lo | hi]: v ~= hi + lo to ~2^-16 relative
+                float hi[32], lo[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  hi[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+                  lo[j] = v[j] - hi[j];
+                }
+                store_row32(p.C2, ARMT_BF16, off2, n0, p.N, p.ldc2, hi);
+                store_row32(p.C2, ARMT_BF16, off2 + p.c2_split, n0, p.N, p.ldc2, lo);
+                store_row32(p.C2, ARMT_BF16, off2 + 2 * p.c2_split, n0, p.N, p.ldc2, hi);
+              } else {
+                store_row32(p.C2, ARMT_BF16, off2, n0, p.N, p.ldc2, v);
+              }
+            }
           } else {
             store_row32(p.C, p.c_dtype, off, n0, p.N, p.ldc, v);
           }
@@ -538,6 +552,7 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   p.C = a.C; p.ldc = a.ldc; p.c_stride = a.c_stride;
   p.R = a.R; p.ldr = a.ldr; p.r_stride = a.r_stride;
   p.C2 = reinterpret_cast<__nv_bfloat16*>(a.C2); p.ldc2 = a.ldc2; p.c2_stride = a.c2_stride;
+  p.c2_split = a.c2_split;
   p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
   p.swiglu_block = a.swiglu_block;

@@ -13,8 +13,10 @@ HBM layout
             (L, d, F), wqa (L, d_mem, d), wkvb (L, Nkvb, d) = [W_v; W_k; W_beta; 0],
             unemb (V, d). F = d_ff padded to a multiple of 32 (zero rows/cols).
   state     A (L, d, d_phi) f32, z (L, d_phi) f32 — the reference MemoryState
-            shapes — plus a bf16 shadow of A (L, d, d_phi_pad) for tensor-core
-            retrieval, refreshed by the fold kernel.
+            shapes — plus (bf16 mode) the memory operand ``memop`` (L, NB, 3P):
+            per layer the [hi|lo|hi] bf16x3 split of A (rows 0..d-1), of z (row
+            d) and of the current member's phi (rows d+8..), the B operand of the
+            tensor-core fold; retrieval reads its hi part. Refreshed by the fold.
   slots     residual stream per in-flight segment: xs (n_slots, T, d) f32 and,
             in bf16 mode, its bf16 copy xs_bf written by the same epilogues.
   members   per-step temporaries stacked over members: h, qkv, ctx, gu, q, phi,
@@ -186,14 +188,15 @@ class MemoryState:
     """Per-layer fast weights on device (armt/memory.py:52-87).
 
     A (L, d, d_phi) f32, z (L, d_phi) f32 (fp32 in both device precisions),
-    updates (L,) int64 on the host (pure bookkeeping). ``shadow`` is the
-    bf16 copy of A the tensor-core retrieval reads; it is derived state.
+    updates (L,) int64 on the host (pure bookkeeping). ``memop`` (bf16 mode)
+    is derived state: the bf16x3 split of A and z read by the tensor-core
+    retrieval and fold (see engine module docstring).
     """
 
     A: torch.Tensor
     z: torch.Tensor
     updates: np.ndarray
-    shadow: torch.Tensor | None = field(default=None, repr=False)
+    memop: torch.Tensor | None = field(default=None, repr=False)
 
     @classmethod
     def fresh(cls, config: ModelConfig, device=None, n_layers: int | None = None) -> "MemoryState":
@@ -231,15 +234,24 @@ class MemoryState:
             raise InputError("memory state tensors must be contiguous")
 
     def sync_shadow(self, prepared: PreparedWeights) -> None:
-        """(Re)build the bf16 copy of A read by tensor-core retrieval (setup
-        work at run start, on the current stream; the fold kernel keeps it
-        in sync afterwards)."""
+        """(Re)build the bf16x3 memory operand from A and z (setup work at run
+        start, on the current stream; the fold keeps it in sync afterwards)."""
         if prepared.dtype_name != "bf16":
             return
         L, d, dphi = self.A.shape
-        if self.shadow is None or tuple(self.shadow.shape) != (L, d, prepared.d_phi_pad):
-            self.shadow = torch.zeros(L, d, prepared.d_phi_pad, dtype=torch.bfloat16, device=self.A.device)
-        self.shadow[:, :, :dphi].copy_(self.A)
+        P = prepared.d_phi_pad
+        nb = int(_lib.load().armt_memop_rows(d, prepared.config.num_mem_tokens))
+        if self.memop is None or tuple(self.memop.shape) != (L, nb, 3 * P):
+            self.memop = torch.zeros(L, nb, 3 * P, dtype=torch.bfloat16, device=self.A.device)
+
+        def split(x):
+            hi = x.to(torch.bfloat16)
+            return hi, (x - hi.float()).to(torch.bfloat16)
+        for rows, src in ((slice(0, d), self.A), (slice(d, d + 1), self.z[:, None, :])):
+            hi, lo = split(src)
+            self.memop[:, rows, 0:dphi] = hi
+            self.memop[:, rows, P:P + dphi] = lo
+            self.memop[:, rows, 2 * P:2 * P + dphi] = hi
 
 
 # ============================================================================
@@ -280,8 +292,11 @@ class Engine:
         self.phi = torch.zeros(G, T, p.d_phi_pad, dtype=wdt, device=dev)
         self.den = torch.empty(G, T, device=dev)
         self.kvb = torch.empty(G, cfg.num_mem_tokens, p.n_kvb, device=dev)
-        nb = int(self.lib.armt_fold_workspace_bytes(G, cfg.num_mem_tokens, p.d_phi))
-        self.fold_ws = torch.empty(max(nb, 16) // 4 + 1, device=dev)
+        if self.bf16:
+            nb = int(self.lib.armt_fold_tc_workspace_bytes(G, cfg.num_mem_tokens, d, p.d_phi))
+        else:
+            nb = int(self.lib.armt_fold_workspace_bytes(G, cfg.num_mem_tokens, p.d_phi))
+        self.fold_ws = torch.zeros(max(nb, 16) // 4 + 1, device=dev)  # zero padding is part of the contract
         self._cache: dict = {}
         self.probe = None   # optional callable(tag, phase) around the gate/up GEMM (bench roofline)
 
@@ -342,13 +357,14 @@ class Engine:
         _lib.check(lib.armt_dpfp_den(mem, self.qm.data_ptr(), T * cfg.d_mem, state.z.data_ptr(),
                                      self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
                                      self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
-        bmat = state.shadow if self.bf16 else state.A
-        ld_b = p.d_phi_pad if self.bf16 else p.d_phi
+        bmat = state.memop if self.bf16 else state.A
+        ld_b = 3 * p.d_phi_pad if self.bf16 else p.d_phi
+        nb_rows = state.memop.shape[1] if self.bf16 else d
 
         def fill_n(a):
-            a.M, a.N, a.K, a.ab_dtype = T, d, ld_b, p.ab
+            a.M, a.N, a.K, a.ab_dtype = T, d, p.d_phi_pad, p.ab
             a.A, a.lda, a.a_stride = self.phi.data_ptr(), p.d_phi_pad, T * p.d_phi_pad
-            a.B, a.ldb, a.b_stride = bmat.data_ptr(), ld_b, d * ld_b
+            a.B, a.ldb, a.b_stride = bmat.data_ptr(), ld_b, nb_rows * ld_b
             a.C, a.ldc, a.c_stride, a.c_dtype = self.xs.data_ptr(), d, T * d, F32
             a.epilogue = EPI_RETRIEVE
             a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
@@ -457,11 +473,16 @@ class Engine:
             self._tables(a, slots, lrel, gid)
         _lib.check(lib.armt_gemm(self._gemm(("kvb", tuple(slots), tuple(layers)), fill_kvb), stream), "kvb")
         mem = self._members(slots, layers)
-        sh = state.shadow if self.bf16 else None
-        _lib.check(lib.armt_mem_fold(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off, p.b_off,
-                                     state.A.data_ptr(), state.z.data_ptr(), _ptr(sh), p.d_phi_pad, d, M,
-                                     cfg.d_mem, cfg.dpfp_nu, p.eps_assoc, self.fold_ws.data_ptr(), stream),
-                   "mem_fold")
+        if self.bf16:
+            _lib.check(lib.armt_mem_fold_tc(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off,
+                                            p.b_off, state.A.data_ptr(), state.z.data_ptr(), state.memop.data_ptr(),
+                                            d, M, cfg.d_mem, cfg.dpfp_nu, p.eps_assoc, self.fold_ws.data_ptr(),
+                                            stream), "mem_fold_tc")
+        else:
+            _lib.check(lib.armt_mem_fold(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off,
+                                         p.b_off, state.A.data_ptr(), state.z.data_ptr(), None, 0, d, M,
+                                         cfg.d_mem, cfg.dpfp_nu, p.eps_assoc, self.fold_ws.data_ptr(), stream),
+                       "mem_fold")
 
     def step(self, slots, layers, state: MemoryState, stream: int) -> None:
         self.retrieve(slots, layers, state, stream)

@@ -79,7 +79,7 @@ def gemm(G, Mr, N, K, epi=_lib.EPI_STORE, c_dtype=BF16, **kw):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--G", type=int, default=16)
-    ap.add_argument("--ops", default="gu,down,qkv,o,kvb,num,attn,fold,lm")
+    ap.add_argument("--ops", default="gu,down,qkv,o,kvb,num,attn,fold,foldtc,lm")
     ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     G = args.G
@@ -105,6 +105,24 @@ def main():
             flops = G * 4 * d * T * (T + 1) / 2
             print(json.dumps({"op": "attn", "G": G, "us": us, "tflops": flops / us / 1e6,
                               "frac_sustained": flops / us / 1e6 / pk["bf16_tflops_sustained"]}), flush=True)
+        elif op == "foldtc":
+            dphi, P = 6 * dm, 6 * dm
+            A = torch.randn(L, d, dphi, device="cuda") * 0.01
+            z = torch.rand(L, dphi, device="cuda") * 10
+            nk = 2128
+            kvb = torch.randn(G, M, nk, device="cuda")
+            nb = LIB.armt_memop_rows(d, M)
+            memop = torch.zeros(L, nb, 3 * P, device="cuda", dtype=torch.bfloat16)
+            ws = torch.zeros(LIB.armt_fold_tc_workspace_bytes(G, M, d, dphi) // 4 + 1, device="cuda")
+            mem = _lib.members(list(range(G)), list(range(G)))
+            s = torch.cuda.current_stream().cuda_stream
+            fn = lambda: _lib.check(LIB.armt_mem_fold_tc(mem, kvb.data_ptr(), nk, M * nk, 0, d, d + dm, A.data_ptr(),
+                                                         z.data_ptr(), memop.data_ptr(), d, M, dm, 3, 100.0,
+                                                         ws.data_ptr(), s), "foldtc")
+            us = timeit(fn, args.iters)
+            byts = G * (2 * d * dphi * 4 + M * nk * 4)
+            print(json.dumps({"op": "foldtc", "G": G, "us": us, "GBps": byts / us / 1e3,
+                              "frac_hbm": byts / us / 1e3 / pk["hbm_gbs"]}), flush=True)
         elif op == "fold":
             dphi = 6 * dm
             A = torch.randn(L, d, dphi, device="cuda") * 0.01

@@ -1,0 +1,118 @@
+"""Summarise ncu outputs into profiles/ (tracked evidence).
+
+    python scripts/profile_summary.py --launches gpurun_out/launches.csv \
+        --full gemm_gu=gpurun_out/gemm_gu.ncu-rep [--full attn=...] --tag r1
+
+Writes profiles/<tag>_launches.md (per-kernel share of device time from the
+cold-cache, serialised launch list) and profiles/<tag>_kernels.json + .md
+(key metrics of each full capture: duration, DRAM bytes, tensor-pipe %, L2 %,
+DRAM %, issue %, registers). bench.py reads the gate/up GEMM's DRAM bytes
+from profiles/*_kernels.json as its roofline `traffic`.
+"""
+
+import argparse
+import collections
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+METRICS = {
+    "duration_ns": "gpu__time_duration.sum",
+    "dram_read_bytes": "dram__bytes_read.sum",
+    "dram_write_bytes": "dram__bytes_write.sum",
+    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram_throughput_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "registers": "launch__registers_per_thread",
+    "grid": "launch__grid_size",
+    "block": "launch__block_size",
+    "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
+}
+
+
+def short(name: str) -> str:
+    name = re.sub(r"\(CUtensorMap_st.*|\(ArmtMembers.*|\(const .*", "", name)
+    name = name.replace("void ", "").replace("armt::", "")
+    return name[:80]
+
+
+def launches(path):
+    text = open(path).read()
+    lines = text.splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
+    h = rows[0]
+    ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        v = float(r[vi].replace(",", ""))
+        unit = r[ui]
+        v *= {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(unit, 1)
+        a = agg[short(r[ki])]
+        a[0] += 1
+        a[1] += v
+    return agg
+
+
+def full_metrics(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, v = rows[0], rows[2] if len(rows) > 2 else rows[1]
+    res = {"kernel": short(v[h.index("Kernel Name")]) if "Kernel Name" in h else ""}
+    for key, m in METRICS.items():
+        if m in h:
+            try:
+                res[key] = float(v[h.index(m)].replace(",", ""))
+            except ValueError:
+                res[key] = v[h.index(m)]
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--launches")
+    ap.add_argument("--full", action="append", default=[])
+    ap.add_argument("--tag", default="r1")
+    ap.add_argument("--note", default="")
+    args = ap.parse_args()
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    if args.launches:
+        agg = launches(args.launches)
+        tot = sum(v[1] for v in agg.values())
+        lines = [f"# {args.tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
+                 args.note, "", f"total device time in capture: {tot / 1e6:.3f} ms", "",
+                 "| share | total ms | launches | avg us | kernel |", "|---:|---:|---:|---:|---|"]
+        for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            lines.append(f"| {v / tot * 100:.1f}% | {v / 1e6:.3f} | {n} | {v / n / 1e3:.1f} | `{k}` |")
+        open(os.path.join(ROOT, "profiles", f"{args.tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+    if args.full:
+        res = {}
+        for item in args.full:
+            label, rep = item.split("=", 1)
+            res[label] = full_metrics(rep)
+        json.dump(res, open(os.path.join(ROOT, "profiles", f"{args.tag}_kernels.json"), "w"), indent=1)
+        lines = [f"# {args.tag}: ncu --set full captures (one launch each)", "", args.note, "",
+                 "| capture | kernel | us | DRAM MB (r+w) | tensor % | L2 % | DRAM % | issue % | regs |",
+                 "|---|---|---:|---:|---:|---:|---:|---:|---:|"]
+        for label, m in res.items():
+            dram = (m.get("dram_read_bytes", 0) + m.get("dram_write_bytes", 0)) / 1e6
+            lines.append(f"| {label} | `{m.get('kernel', '')}` | {m.get('duration_ns', 0) / 1e3:.1f} | {dram:.1f} | "
+                         f"{m.get('tensor_pipe_pct', 0):.1f} | {m.get('l2_throughput_pct', 0):.1f} | "
+                         f"{m.get('dram_throughput_pct', 0):.1f} | {m.get('issue_active_pct', 0):.1f} | "
+                         f"{m.get('registers', 0):.0f} |")
+        open(os.path.join(ROOT, "profiles", f"{args.tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
