@@ -189,22 +189,40 @@ __global__ void __launch_bounds__(256) fold_chain_kernel(const __grid_constant__
       const int t = lane + 32 * r;
       e[r] = t < M ? cg[t] : 0.f;
     }
-    for (int i = 0; i < M; ++i) {
-      const int owner = i & 31, qi = i >> 5;
+    // blocks of 4 tokens: every lane redundantly runs the 4-step scalar chain
+    // (4 shuffles in parallel, K entries as smem broadcasts), then all owned
+    // tokens absorb the block's 4 gammas at once.
+    for (int i0 = 0; i0 < M; i0 += 4) {
+      const int qi = i0 >> 5, l0 = i0 & 31;
       float mine = 0.f;
 #pragma unroll
       for (int r = 0; r < QMAX; ++r)
         if (r == qi) mine = e[r];
-      const float zq = __shfl_sync(0xffffffffu, mine, owner);
-      const float nrm = snrm[i];
-      const float gam = nrm <= eps ? 0.f : 1.f - zq / nrm;
-      if (lane == owner) { szq[i] = zq; sgam[i] = gam; }
-      // K_ti read as row i of K (lanes walk t: consecutive words, no bank conflicts)
+      float zq[4], gam[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zq[u] = __shfl_sync(0xffffffffu, mine, l0 + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+#pragma unroll
+        for (int v = 0; v < u; ++v) zq[u] = fmaf(gam[v], sK[(i0 + v) * Mp + i], zq[u]);
+        const float nrm = i < M ? snrm[i] : 0.f;
+        gam[u] = (i < M && nrm > eps) ? 1.f - zq[u] / nrm : 0.f;
+      }
+      if (lane < 4 && i0 + lane < M) {
+        szq[i0 + lane] = lane == 0 ? zq[0] : lane == 1 ? zq[1] : lane == 2 ? zq[2] : zq[3];
+        sgam[i0 + lane] = lane == 0 ? gam[0] : lane == 1 ? gam[1] : lane == 2 ? gam[2] : gam[3];
+      }
 #pragma unroll
       for (int r = 0; r < QMAX; ++r) {
         if (r < rmax) {
           const int t = lane + 32 * r;
-          if (t > i && t < M) e[r] = fmaf(gam, sK[i * Mp + t], e[r]);
+          if (t >= i0 + 4 && t < M) {
+            float acc = e[r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = fmaf(gam[u], sK[(i0 + u) * Mp + t], acc);
+            e[r] = acc;
+          }
         }
       }
     }
