@@ -11,6 +11,7 @@
 //    with cp.async, heaviest (last) query blocks scheduled first.
 //  * f32:  SIMT online softmax for the 1e-4 parity mode.
 
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace armt {
@@ -313,6 +314,10 @@ static int launch_bf16(int G, const void* qkv, long long ld_qkv, long long qkv_s
 }  // namespace attn
 }  // namespace armt
 
+namespace armt {
+int attention_tc(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx, long long ld_ctx,
+                 long long ctx_stride, int T, int H, int dh, float scale, cudaStream_t s);
+}
 using namespace armt;
 
 extern "C" int armt_attention(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx,
@@ -334,6 +339,13 @@ extern "C" int armt_attention(int G, const void* qkv, long long ld_qkv, long lon
   }
   ARMT_REQUIRE(dh % 8 == 0 && ld_qkv % 8 == 0 && ld_ctx % 2 == 0, ARMT_ERR_DIM,
                "attention bf16: head dim and row strides must be multiples of 8");
+  // tcgen05 kernel for d_head 64/128 (ARMT_ATTN=mma forces the mma.sync kernel for A/B runs)
+  static const bool force_mma = [] {
+    const char* e = getenv("ARMT_ATTN");
+    return e != nullptr && e[0] == 'm';
+  }();
+  if ((dh == 64 || dh == 128) && !force_mma)
+    return attention_tc(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 16) return launch_bf16<16>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 32) return launch_bf16<32>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 64) return launch_bf16<64>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
