@@ -72,6 +72,12 @@ typedef struct {
   const float* R; long long ldr, r_stride;     /* RESIDUAL/RETRIEVE input, indexed by c_slot */
   void* C2; long long ldc2, c2_stride;         /* RESIDUAL: optional bf16 copy, indexed by c_slot */
   int c2_split;                         /* >0: C2 gets [hi | lo | hi] bf16 split of C at cols n, n+s, n+2s */
+  /* fused RMSNorm (bf16 path): RESIDUAL/RETRIEVE epilogues write sum(C^2) of each row per
+   * 64-column block to ssq_out[g*ssq_stride + m*ssq_np + n/64]; ROPE/SWIGLU epilogues scale
+   * the accumulator row by 1/sqrt(sum_p ssq_in[g*ssq_stride + m*ssq_np + p]/norm_d + norm_eps),
+   * summing the ssq_np partials in order (deterministic: no atomics). */
+  float* ssq_out; const float* ssq_in; long long ssq_stride; int ssq_np;
+  int norm_d; float norm_eps;
   const float* den; long long den_stride;      /* RETRIEVE: den[g*den_stride + m] */
   float eps;
   const float* rope_cos; const float* rope_sin;  /* ROPE: (head_dim/2, M) tables, position-contiguous */

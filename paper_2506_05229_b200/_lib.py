@@ -48,6 +48,8 @@ class ArmtGemmArgs(ctypes.Structure):
         ("R", _P), ("ldr", _LL), ("r_stride", _LL),
         ("C2", _P), ("ldc2", _LL), ("c2_stride", _LL),
         ("c2_split", _I),
+        ("ssq_out", _P), ("ssq_in", _P), ("ssq_stride", _LL), ("ssq_np", _I),
+        ("norm_d", _I), ("norm_eps", _F),
         ("den", _P), ("den_stride", _LL),
         ("eps", _F),
         ("rope_cos", _P), ("rope_sin", _P),

@@ -44,6 +44,7 @@ struct Params {
   void* C; long long ldc, c_stride;
   const float* R; long long ldr, r_stride;
   __nv_bfloat16* C2; long long ldc2, c2_stride; int c2_split;
+  float* ssq_out; const float* ssq_in; long long ssq_stride; int ssq_np; int norm_d; float norm_eps;
   const float* den; long long den_stride;
   float eps;
   const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
@@ -230,6 +231,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
+      // fused RMSNorm of the A rows: acc * 1/sqrt(mean(x^2) + eps) (gains live in the weights)
+      float rs = 1.f;
+      if constexpr (EPI == E_SWIGLU || EPI == E_ROPE) {
+        if (p.ssq_in != nullptr && live) {
+          const float* part = p.ssq_in + (long long)g * p.ssq_stride + (long long)row * p.ssq_np;
+          float t = 0.f;
+          int q = 0;
+          if ((p.ssq_np & 3) == 0) {  // float4 loads, all issued before the (fixed-order) sum
+            float4 v[8];
+            for (; q + 32 <= p.ssq_np; q += 32) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = reinterpret_cast<const float4*>(part + q)[u];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) t += ((v[u].x + v[u].y) + (v[u].z + v[u].w));
+            }
+            for (; q < p.ssq_np; q += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(part + q);
+              t += ((w4.x + w4.y) + (w4.z + w4.w));
+            }
+          }
+          for (; q < p.ssq_np; ++q) t += part[q];  // fixed order: deterministic
+          rs = 1.f / sqrtf(t / (float)p.norm_d + p.norm_eps);
+        }
+      }
 
       if constexpr (EPI == E_SWIGLU) {
         const int out_n0 = nb * (BN / 2);
@@ -240,7 +265,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tmem_ld32(tbase + c0, gte);
           tmem_ld32(tbase + BN / 2 + c0, up);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) gte[j] = gte[j] * __frcp_rn(1.f + __expf(-gte[j])) * up[j];
+          for (int j = 0; j < 32; ++j) {
+            const float gv = gte[j] * rs;
+            gte[j] = gv * __frcp_rn(1.f + __expf(-gv)) * (up[j] * rs);
+          }
           if (live && out_n0 + c0 < p.N / 2) store_row32(p.C, ARMT_BF16, off, out_n0 + c0, p.N / 2, p.ldc, gte);
         }
       } else if constexpr (EPI == E_ROPE) {
@@ -262,6 +290,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               tmem_ld32(tbase + c0 + 32 * q, x1);
               tmem_ld32(tbase + c0 + DH / 2 + 32 * q, x2);
               if (live && n0 < p.N) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) { x1[j] *= rs; x2[j] *= rs; }
                 if (rot) {
 #pragma unroll
                   for (int j = 0; j < 32; ++j) {
@@ -280,6 +310,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             __syncwarp();
             tmem_ld32(tbase + c0, x);
             if (live && n0 < p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) x[j] *= rs;
               if (rot) rope_chunk<DH, 32>(x, cos_col, sin_col, p.M);
               store_row32(p.C, ARMT_BF16, off, n0, p.N, p.ldc, x);
             }
@@ -287,6 +319,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       } else {
         float rden = 1.f; bool guarded = false;
+        float ssq = 0.f;
         if constexpr (EPI == E_RETRIEVE) {
           const float den = live ? p.den[(long long)g * p.den_stride + row] : 1.f;
           guarded = fabsf(den) <= p.eps;
@@ -310,7 +343,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               else v[j] = res[j] + v[j];
             }
             store_row32(p.C, ARMT_F32, off, n0, p.N, p.ldc, v);
-            if (EPI == E_RESIDUAL && p.C2 != nullptr) {
+            if (p.ssq_out != nullptr) {
+              // partial sum of squares per 64-column block (two 32-column chunks)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) ssq = (n0 + j < p.N) ? fmaf(v[j], v[j], ssq) : ssq;
+              if ((n0 & 63) == 32 || n0 + 32 >= p.N) {
+                p.ssq_out[(long long)g * p.ssq_stride + (long long)row * p.ssq_np + (n0 >> 6)] = ssq;
+                ssq = 0.f;
+              }
+            }
+            if (p.C2 != nullptr) {
               const long long off2 = (long long)c_slot * p.c2_stride + (long long)row * p.ldc2;
               if (p.c2_split > 0) {
                 // bf16x3 operand layout [hi | lo | hi]: v ~= hi + lo to ~2^-16 relative
@@ -483,6 +525,8 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   p.R = a.R; p.ldr = a.ldr; p.r_stride = a.r_stride;
   p.C2 = reinterpret_cast<__nv_bfloat16*>(a.C2); p.ldc2 = a.ldc2; p.c2_stride = a.c2_stride;
   p.c2_split = a.c2_split;
+  p.ssq_out = a.ssq_out; p.ssq_in = a.ssq_in; p.ssq_stride = a.ssq_stride; p.ssq_np = a.ssq_np;
+  p.norm_d = a.norm_d; p.norm_eps = a.norm_eps;
   p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
   p.swiglu_block = a.swiglu_block;

@@ -72,8 +72,9 @@ class PreparedWeights:
     wo: torch.Tensor
     wgu: torch.Tensor
     wdown: torch.Tensor
-    attn_gain: torch.Tensor
+    attn_gain: torch.Tensor       # (folded into wqkv / wgu; kept for inspection)
     mlp_gain: torch.Tensor
+    unit_gain: torch.Tensor       # ones: the stand-alone RMSNorm applies no gain (it is in the weights)
     wqa: torch.Tensor
     wkvb: torch.Tensor
     unemb: torch.Tensor
@@ -139,13 +140,15 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
     def kmajor(t):  # (L, in, out) -> (L, out, in)
         return t.transpose(1, 2).contiguous()
 
-    wqkv = kmajor(torch.cat([up("wq"), up("wk"), up("wv")], dim=2)).to(wdt)
+    # RMSNorm gains fold into the consuming weights: (x/r * g) @ W = (x/r) @ (diag(g) W)
+    g_attn, g_mlp = up("attn_gain"), up("mlp_gain")
+    wqkv = kmajor(torch.cat([up("wq"), up("wk"), up("wv")], dim=2) * g_attn[:, :, None]).to(wdt)
     wo = kmajor(up("wo")).to(wdt)
     Ls = hi - lo
     gate = torch.zeros(Ls, d, d_ff_pad, device=dev)
     upw = torch.zeros(Ls, d, d_ff_pad, device=dev)
-    gate[:, :, :dff] = up("w_gate")
-    upw[:, :, :dff] = up("w_in")
+    gate[:, :, :dff] = up("w_gate") * g_mlp[:, :, None]
+    upw[:, :, :dff] = up("w_in") * g_mlp[:, :, None]
     nt = d_ff_pad // block
     gu = torch.stack([gate.view(Ls, d, nt, block), upw.view(Ls, d, nt, block)], dim=3)
     wgu = kmajor(gu.reshape(Ls, d, 2 * d_ff_pad)).to(wdt)
@@ -166,7 +169,8 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
         d_ff_pad=d_ff_pad, swiglu_block=block, n_kvb=n_kvb,
         embedding=up("embedding", False).to(wdt), mem_embedding=up("mem_embedding", False).to(wdt),
         wqkv=wqkv, wo=wo, wgu=wgu, wdown=wdown,
-        attn_gain=up("attn_gain").contiguous(), mlp_gain=up("mlp_gain").contiguous(),
+        attn_gain=g_attn.contiguous(), mlp_gain=g_mlp.contiguous(),
+        unit_gain=torch.ones_like(g_attn).contiguous(),
         wqa=up("w_q_assoc").to(wdt).contiguous(), wkvb=wkvb.to(wdt),
         unemb=up("unembedding", False).t().contiguous().to(wdt),
         rope_cos=torch.as_tensor(np.cos(ang), dtype=torch.float32).to(dev).contiguous(),
@@ -268,7 +272,7 @@ class Engine:
     """
 
     def __init__(self, prepared: PreparedWeights, max_members: int, n_slots: int,
-                 n_state_layers: int | None = None):
+                 n_state_layers: int | None = None, fused_norm: bool = True):
         p = prepared
         cfg = p.config
         self.p = p
@@ -297,6 +301,12 @@ class Engine:
         else:
             nb = int(self.lib.armt_fold_workspace_bytes(G, cfg.num_mem_tokens, p.d_phi))
         self.fold_ws = torch.zeros(max(nb, 16) // 4 + 1, device=dev)  # zero padding is part of the contract
+        # fused RMSNorm (bf16, full step path): per-row sum of squares produced by the
+        # residual epilogues, consumed (and re-zeroed) by the next GEMM's epilogue
+        self.fused = self.bf16 and fused_norm
+        self.ssq_np = (d + 63) // 64
+        self.ssq_attn = torch.zeros(G, T, self.ssq_np, device=dev)
+        self.ssq_mlp = torch.zeros(G, T, self.ssq_np, device=dev)
         self._cache: dict = {}
         self.probe = None   # optional callable(tag, phase) around the gate/up GEMM (bench roofline)
 
@@ -369,6 +379,9 @@ class Engine:
             a.epilogue = EPI_RETRIEVE
             a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
             a.den, a.den_stride, a.eps = self.den.data_ptr(), T, p.eps_assoc
+            if self.fused:
+                a.C2, a.ldc2, a.c2_stride = self.xs_bf.data_ptr(), d, T * d
+                a.ssq_out, a.ssq_stride, a.ssq_np = self.ssq_attn.data_ptr(), T * self.ssq_np, self.ssq_np
             self._tables(a, gid, lrel, slots)
         args = self._gemm(("num", tuple(slots), tuple(layers), bmat.data_ptr()), fill_n)
         _lib.check(lib.armt_gemm(args, stream), "retrieve numerator")
@@ -379,25 +392,32 @@ class Engine:
         T, d, G = p.T, cfg.d_model, len(layers)
         lrel = [l - self.layer_base for l in layers]
         gid = list(range(G))
-        key = (tuple(slots), tuple(layers))
+        key = (tuple(slots), tuple(layers), self.fused)
         mem = self._members(slots, layers)
         wout = BF16 if self.bf16 else F32
-        # attention sub-block
-        _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.attn_gain.data_ptr(), self.h.data_ptr(),
-                                    wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm attn")
+        fused = self.fused
+        # attention sub-block: RMSNorm fused into the QKV epilogue (bf16) or stand-alone
+        if not fused:
+            _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.unit_gain.data_ptr(), self.h.data_ptr(),
+                                        wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm attn")
+        a_in = self.xs_bf if fused else self.h
+        a_idx = slots if fused else gid
 
         def fill_qkv(a):
             a.M, a.N, a.K, a.ab_dtype = T, 3 * d, d, p.ab
-            a.A, a.lda, a.a_stride = self.h.data_ptr(), d, T * d
+            a.A, a.lda, a.a_stride = a_in.data_ptr(), d, T * d
             a.B, a.ldb, a.b_stride = p.wqkv.data_ptr(), d, 3 * d * d
             a.C, a.ldc, a.c_stride, a.c_dtype = self.qkv.data_ptr(), 3 * d, T * 3 * d, wout
             if self.bf16:
                 a.epilogue = EPI_ROPE
                 a.rope_cos, a.rope_sin = p.rope_cos_t.data_ptr(), p.rope_sin_t.data_ptr()
                 a.head_dim, a.rope_cols = p.d_head, 2 * d
+                if fused:
+                    a.ssq_in, a.ssq_stride, a.ssq_np = self.ssq_attn.data_ptr(), T * self.ssq_np, self.ssq_np
+                    a.norm_d, a.norm_eps = d, cfg.eps_norm
             else:
                 a.epilogue = EPI_STORE
-            self._tables(a, gid, lrel, gid)
+            self._tables(a, a_idx, lrel, gid)
         _lib.check(lib.armt_gemm(self._gemm(("qkv",) + key, fill_qkv), stream), "qkv")
         if not self.bf16:
             _lib.check(lib.armt_rope(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, F32, T, cfg.n_heads, p.d_head,
@@ -413,25 +433,32 @@ class Engine:
             a.C, a.ldc, a.c_stride, a.c_dtype = self.xs.data_ptr(), d, T * d, F32
             a.epilogue = EPI_RESIDUAL
             a.R, a.ldr, a.r_stride = self.xs.data_ptr(), d, T * d
+            if fused:
+                a.C2, a.ldc2, a.c2_stride = self.xs_bf.data_ptr(), d, T * d
+                a.ssq_out, a.ssq_stride, a.ssq_np = self.ssq_mlp.data_ptr(), T * self.ssq_np, self.ssq_np
             self._tables(a, gid, lrel, slots)
         _lib.check(lib.armt_gemm(self._gemm(("o",) + key, fill_o), stream), "o-proj")
         # MLP sub-block
-        _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.mlp_gain.data_ptr(), self.h.data_ptr(),
-                                    wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm mlp")
+        if not fused:
+            _lib.check(lib.armt_rmsnorm(mem, self.xs.data_ptr(), T * d, p.unit_gain.data_ptr(), self.h.data_ptr(),
+                                        wout, T * d, T, d, cfg.eps_norm, stream), "rmsnorm mlp")
         F = p.d_ff_pad
 
         def fill_gu(a):
             a.M, a.N, a.K, a.ab_dtype = T, 2 * F, d, p.ab
-            a.A, a.lda, a.a_stride = self.h.data_ptr(), d, T * d
+            a.A, a.lda, a.a_stride = a_in.data_ptr(), d, T * d
             a.B, a.ldb, a.b_stride = p.wgu.data_ptr(), d, 2 * F * d
             if self.bf16:
                 a.C, a.ldc, a.c_stride, a.c_dtype = self.gu.data_ptr(), F, T * F, BF16
                 a.epilogue = EPI_SWIGLU
                 a.swiglu_block = p.swiglu_block
+                if fused:
+                    a.ssq_in, a.ssq_stride, a.ssq_np = self.ssq_mlp.data_ptr(), T * self.ssq_np, self.ssq_np
+                    a.norm_d, a.norm_eps = d, cfg.eps_norm
             else:
                 a.C, a.ldc, a.c_stride, a.c_dtype = self.gu_full.data_ptr(), 2 * F, T * 2 * F, F32
                 a.epilogue = EPI_STORE
-            self._tables(a, gid, lrel, gid)
+            self._tables(a, a_idx, lrel, gid)
         if self.probe is not None:
             self.probe(G, 0)
         _lib.check(lib.armt_gemm(self._gemm(("gu",) + key, fill_gu), stream), "gate/up")

@@ -44,7 +44,9 @@ def _engine(prepared: PreparedWeights, G: int) -> Engine:
     cache = prepared.__dict__.setdefault("_engines", {})
     eng = cache.get(G)
     if eng is None:
-        eng = Engine(prepared, G, G)
+        # the per-core API runs forward_stack without a preceding retrieve epilogue,
+        # so it uses the stand-alone RMSNorm rather than the fused row statistics
+        eng = Engine(prepared, G, G, fused_norm=False)
         cache[G] = eng
     return eng
 

@@ -69,6 +69,19 @@ def test_device_schedules_agree_bitwise(c1, dtype):
     assert torch.equal(s1.A, s2.A) and torch.equal(s1.z, s2.z)
 
 
+def test_mid_width_runs_are_deterministic_and_schedule_invariant():
+    # d=256 spans several N tiles per row: exercises the fused-RMSNorm partial
+    # sums (fixed-order, no atomics) for bitwise reproducibility
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    prep = prepare_weights(conditioned_weights(cfg), "bf16")
+    tokens = cli_tokens(cfg, 5 * cfg.segment_size, seed=8)
+    a, _ = run_diagonal(prep, cfg, tokens)
+    b, _ = run_diagonal(prep, cfg, tokens)
+    c, _ = run_sequential(prep, cfg, tokens)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, c)
+
+
 def test_shuffle_and_graph_do_not_change_logits(c1):
     cfg, _, prep = c1
     tokens = cli_tokens(cfg, 6 * cfg.segment_size, seed=4)
