@@ -57,6 +57,21 @@ def run_flops(cfg, n_segments: int) -> float:
     return n_segments * cfg.n_layers * cell_flops(cfg) + 2 * n_segments * cfg.segment_size * cfg.d_model * cfg.vocab_size
 
 
+def load_traffic():
+    """DRAM bytes per gate/up launch from the committed ncu --set full capture
+    (profiles/*_kernels.json, written by scripts/profile_summary.py)."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json"))):
+        try:
+            m = json.load(open(path)).get("gemm_gu")
+        except (OSError, ValueError):
+            continue
+        if m and "dram_read_bytes" in m:
+            best = {"bytes": m["dram_read_bytes"] + m.get("dram_write_bytes", 0), "source": os.path.basename(path)}
+    return best
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -291,6 +306,9 @@ def device_arm(args, rank, world):
     mean_nll = float(host_nll.mean()) if rank == world - 1 else None
 
     peaks, peak_kind = load_peaks()
+    traffic = load_traffic()
+    gu_bytes = 2.0 * (full_g * cfg.tokens_per_segment * cfg.d_model + full_g * 2 * sess.p.d_ff_pad * cfg.d_model
+                      + full_g * cfg.tokens_per_segment * sess.p.d_ff_pad)
     # dominant kernel: the grouped tcgen05 GEMM; probed launch = full-width gate/up (SwiGLU epilogue)
     gu_flops = 2.0 * full_g * cfg.tokens_per_segment * (2 * sess.p.d_ff_pad) * cfg.d_model
     n_probe = len(probe_events)
@@ -321,7 +339,10 @@ def device_arm(args, rank, world):
                    "whole_step_frac_of_sustained": step_tflops / peaks.get("bf16_tflops_sustained", peak),
                    "setup_s": setup_s},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": (traffic or {}).get("bytes"),
+                     "traffic_note": (f"DRAM bytes per launch (read+write) from {traffic['source']}; algorithmic "
+                                      f"operand+output bytes {gu_bytes / 1e9:.3f} GB" if traffic else None),
                      "kernel": f"tcgen05 grouped GEMM, gate/up (SwiGLU epilogue), G={full_g}, "
                                f"{gu_flops / 1e12:.3f} TFLOP/launch, {n_probe} launches/step",
                      "peak_kind": f"{peak_kind} bf16_tflops_sustained"},
