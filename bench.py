@@ -277,7 +277,15 @@ def device_arm(args, rank, world):
     ms_per_step = total_ms / args.steps
     value = n / (ms_per_step / 1e3)
 
-    # end-to-end through the public scoring API: pinned H2D ids + D2H per-token NLL each step
+    # end-to-end through the public scoring API: pinned H2D ids + D2H per-token NLL each step.
+    # Single GPU: a scoring Session fuses the next-token NLL into the LM-head epilogue
+    # (no 33.6 GB logits round trip); the sharded path scores from the last rank's logits.
+    launches_per_forward = sess.kernels_per_forward
+    if world == 1:
+        del sess
+        torch.cuda.empty_cache()
+        sess = Session(prep, n, schedule=args.schedule, scoring=True)
+        sess.warm()
     host_ids = torch.as_tensor(tokens).pin_memory()
     host_nll = torch.empty(n - 1, dtype=torch.float32).pin_memory()
     for _ in range(2):
@@ -307,10 +315,11 @@ def device_arm(args, rank, world):
 
     peaks, peak_kind = load_peaks()
     traffic = load_traffic()
-    gu_bytes = 2.0 * (full_g * cfg.tokens_per_segment * cfg.d_model + full_g * 2 * sess.p.d_ff_pad * cfg.d_model
-                      + full_g * cfg.tokens_per_segment * sess.p.d_ff_pad)
+    d_ff_pad = sess.p.d_ff_pad
+    gu_bytes = 2.0 * (full_g * cfg.tokens_per_segment * cfg.d_model + full_g * 2 * d_ff_pad * cfg.d_model
+                      + full_g * cfg.tokens_per_segment * d_ff_pad)
     # dominant kernel: the grouped tcgen05 GEMM; probed launch = full-width gate/up (SwiGLU epilogue)
-    gu_flops = 2.0 * full_g * cfg.tokens_per_segment * (2 * sess.p.d_ff_pad) * cfg.d_model
+    gu_flops = 2.0 * full_g * cfg.tokens_per_segment * (2 * d_ff_pad) * cfg.d_model
     n_probe = len(probe_events)
     probe_avg_ms = statistics.mean(probe_ms) / max(n_probe, 1)
     achieved = gu_flops / (probe_avg_ms / 1e3) / 1e12 if n_probe else None
@@ -348,9 +357,11 @@ def device_arm(args, rank, world):
                      "peak_kind": f"{peak_kind} bf16_tflops_sustained"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(n * 8),
-                "d2h_bytes_per_step": int((n - 1) * 4), "api": "Session.nll (pinned ids in, per-token NLL out)",
+                "d2h_bytes_per_step": int((n - 1) * 4),
+                "api": "Session(scoring=True).nll: pinned ids in, per-token NLL out (LM-head fused NLL)"
+                       if world == 1 else "ShardedSession.nll: pinned ids in, per-token NLL out",
                 "mean_nll": mean_nll},
-        "gpu_launches": int(sess.kernels_per_forward * args.steps),
+        "gpu_launches": int(launches_per_forward * args.steps),
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)

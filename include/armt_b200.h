@@ -46,7 +46,10 @@ typedef enum {
   ARMT_EPI_RESIDUAL = 1,  /* C = R + acc (f32); optional C2 = bf16(C)                 */
   ARMT_EPI_RETRIEVE = 2,  /* C = R + (|den| <= eps ? 0 : acc/den)  armt/memory.py:149-152 */
   ARMT_EPI_SWIGLU = 3,    /* C[:, j] = silu(acc_gate) * acc_up     armt/layers.py:228-232 */
-  ARMT_EPI_ROPE = 4       /* C = rope(acc) on cols < rope_cols     armt/layers.py:169-176 */
+  ARMT_EPI_ROPE = 4,      /* C = rope(acc) on cols < rope_cols     armt/layers.py:169-176 */
+  ARMT_EPI_LSE = 5        /* no C: per row and N-tile (max, sum exp) of acc in base-2 units into
+                             lse_part[row*lse_ld + nb] (float2), and acc[row][targets[row]] into
+                             lse_tgt[row] -- the fused next-token NLL of the LM head */
 } ArmtEpilogue;
 
 /* Members of one grouped launch: member g runs slot[g] against layer[g]. */
@@ -78,6 +81,7 @@ typedef struct {
    * summing the ssq_np partials in order (deterministic: no atomics). */
   float* ssq_out; const float* ssq_in; long long ssq_stride; int ssq_np;
   int norm_d; float norm_eps;
+  float* lse_part; long long lse_ld; const long long* targets; float* lse_tgt; int lse_rows;
   const float* den; long long den_stride;      /* RETRIEVE: den[g*den_stride + m] */
   float eps;
   const float* rope_cos; const float* rope_sin;  /* ROPE: (head_dim/2, M) tables, position-contiguous */
@@ -160,6 +164,11 @@ int armt_cast(const void* src, int src_dtype, void* dst, int dst_dtype, long lon
  * Used by the end-to-end API to return a scalar result to the host. */
 int armt_logits_nll(const void* logits, int dtype, long long ld, const long long* targets,
                     float* nll, long long rows, int vocab, void* stream);
+
+/* Finalize the fused LM-head NLL: nll[r] = ln2 * (M + log2(sum_t s_t 2^(m_t - M))) - tgt[r],
+ * M = max_t m_t over the n_tiles (max, sum) partials of row r (rows with target < 0 -> 0). */
+int armt_lse_finalize(const float* lse_part, long long lse_ld, int n_tiles, const float* tgt,
+                      const long long* targets, float* nll, long long rows, void* stream);
 
 /* Introspection. */
 const char* armt_last_error(void);

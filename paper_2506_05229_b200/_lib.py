@@ -18,14 +18,14 @@ LIB_PATH = os.path.join(HERE, "libarmt_b200.so")
 
 MAX_MEMBERS = 128
 F32, BF16 = 0, 1
-EPI_STORE, EPI_RESIDUAL, EPI_RETRIEVE, EPI_SWIGLU, EPI_ROPE = 0, 1, 2, 3, 4
+EPI_STORE, EPI_RESIDUAL, EPI_RETRIEVE, EPI_SWIGLU, EPI_ROPE, EPI_LSE = 0, 1, 2, 3, 4, 5
 
 # Every symbol the header declares (checked by tests/test_boundary.py).
 EXPORTS = ("armt_gemm", "armt_embed", "armt_rmsnorm", "armt_dpfp_den", "armt_attention",
            "armt_rope", "armt_swiglu", "armt_mem_fold", "armt_fold_workspace_bytes", "armt_cast",
            "armt_logits_nll", "armt_last_error", "armt_version", "armt_num_sms",
            "armt_kernel_count", "armt_abi_sizeof", "armt_mem_fold_tc", "armt_fold_tc_workspace_bytes",
-           "armt_memop_rows")
+           "armt_memop_rows", "armt_lse_finalize")
 
 _I = ctypes.c_int
 _LL = ctypes.c_longlong
@@ -50,6 +50,7 @@ class ArmtGemmArgs(ctypes.Structure):
         ("c2_split", _I),
         ("ssq_out", _P), ("ssq_in", _P), ("ssq_stride", _LL), ("ssq_np", _I),
         ("norm_d", _I), ("norm_eps", _F),
+        ("lse_part", _P), ("lse_ld", _LL), ("targets", _P), ("lse_tgt", _P), ("lse_rows", _I),
         ("den", _P), ("den_stride", _LL),
         ("eps", _F),
         ("rope_cos", _P), ("rope_sin", _P),
@@ -89,6 +90,7 @@ def load(path: str = LIB_PATH):
                                   _I, _I, _I, _I, _F, _P, _P]),
         "armt_fold_tc_workspace_bytes": (_LL, [_I, _I, _I, _I]),
         "armt_memop_rows": (_LL, [_I, _I]),
+        "armt_lse_finalize": (_I, [_P, _LL, _I, _P, _P, _P, _LL, _P]),
         "armt_cast": (_I, [_P, _I, _P, _I, _LL, _P]),
         "armt_logits_nll": (_I, [_P, _I, _LL, _P, _P, _LL, _I, _P]),
         "armt_last_error": (ctypes.c_char_p, []),

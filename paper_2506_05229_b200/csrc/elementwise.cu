@@ -197,6 +197,26 @@ __global__ void __launch_bounds__(256) nll_kernel(const T* __restrict__ logits, 
   }
 }
 
+// Fused-NLL finalize: combine the per-tile (max, sum 2^x) partials of each row.
+__global__ void lse_finalize_kernel(const float2* __restrict__ part, long long ld, int n_tiles,
+                                    const float* __restrict__ tgt, const long long* __restrict__ targets,
+                                    float* __restrict__ nll, long long rows) {
+  const long long row = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float2* pr = part + row * ld;
+  float M = -INFINITY;
+  for (int t = lane; t < n_tiles; t += 32) M = fmaxf(M, pr[t].x);
+  M = warp_max(M);
+  float S = 0.f;
+  for (int t = lane; t < n_tiles; t += 32) {
+    const float2 q = pr[t];
+    S += q.y * exp2f(q.x - M);
+  }
+  S = warp_sum(S);
+  if (lane == 0) nll[row] = targets[row] < 0 ? 0.f : 0.6931471805599453f * (M + log2f(S) - tgt[row]);
+}
+
 }  // namespace armt
 
 using namespace armt;
@@ -304,6 +324,15 @@ int armt_logits_nll(const void* logits, int dtype, long long ld, const long long
     nll_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(reinterpret_cast<const float*>(logits), ld, targets,
                                                               nll, vocab);
   ARMT_CHECK_LAUNCH("nll");
+  return ARMT_OK;
+}
+
+int armt_lse_finalize(const float* lse_part, long long lse_ld, int n_tiles, const float* tgt,
+                      const long long* targets, float* nll, long long rows, void* stream) {
+  if (rows <= 0) return ARMT_OK;
+  lse_finalize_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float2*>(lse_part), lse_ld, n_tiles, tgt, targets, nll, rows);
+  ARMT_CHECK_LAUNCH("lse_finalize");
   return ARMT_OK;
 }
 

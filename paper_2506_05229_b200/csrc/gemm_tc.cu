@@ -45,6 +45,7 @@ struct Params {
   const float* R; long long ldr, r_stride;
   __nv_bfloat16* C2; long long ldc2, c2_stride; int c2_split;
   float* ssq_out; const float* ssq_in; long long ssq_stride; int ssq_np; int norm_d; float norm_eps;
+  float2* lse_part; long long lse_ld; const long long* targets; float* lse_tgt; int lse_rows;
   const float* den; long long den_stride;
   float eps;
   const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
@@ -66,7 +67,13 @@ template <int BN> struct Cfg {
 using namespace tcx;
 
 // ---------------------------------------------------------------- epilogues
-enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4 };
+enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4, E_LSE = 5 };
+
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Store 32 consecutive values of one row starting at column n0 (< N).
 __device__ __forceinline__ void store_row32(void* base, int dtype, long long off, int n0, int N,
@@ -256,7 +263,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       }
 
-      if constexpr (EPI == E_SWIGLU) {
+      if constexpr (EPI == E_LSE) {
+        // fused next-token NLL: online (max, sum 2^x) of the row's logits in base 2
+        constexpr float LOG2E = 1.4426950408889634f;
+        float m = -INFINITY, ssum = 0.f, tv = 0.f;
+        const long long tgt = (live && row < p.lse_rows) ? p.targets[row] : -1;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          const int n0 = nb * BN + c0;
+          float cm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = (n0 + j < p.N) ? v[j] * LOG2E : -INFINITY;
+            cm = fmaxf(cm, v[j]);
+            if (n0 + j == tgt) tv = v[j];
+          }
+          const float mn = fmaxf(m, cm);
+          if (mn == -INFINITY) continue;  // whole chunk past N
+          float cs = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) cs += fast_exp2(v[j] - mn);
+          ssum = (m == -INFINITY ? 0.f : ssum * fast_exp2(m - mn)) + cs;
+          m = mn;
+        }
+        if (live && row < p.lse_rows) {
+          p.lse_part[(long long)row * p.lse_ld + nb] = make_float2(m, ssum);
+          if (tgt >= (long long)nb * BN && tgt < (long long)nb * BN + BN) p.lse_tgt[row] = tv;
+        }
+      } else if constexpr (EPI == E_SWIGLU) {
         const int out_n0 = nb * (BN / 2);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN / 2; c0 += 32) {
@@ -441,6 +478,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
 
 static int pick_bn(const ArmtGemmArgs& a) {
   if (a.epilogue == ARMT_EPI_SWIGLU) return 2 * a.swiglu_block;
+  if (a.epilogue == ARMT_EPI_LSE) return 256;  // lse_ld = ceil(N / 256) partials per row
   const int sms = num_sms();
   const long long tm = (a.M + BM - 1) / BM;
   const bool rope = a.epilogue == ARMT_EPI_ROPE;
@@ -467,6 +505,9 @@ static int dispatch_epi(const ArmtGemmArgs& a, const CUtensorMap& ma, const CUte
     case ARMT_EPI_STORE: return launch<BN, E_STORE, 0>(ma, mb, p, s);
     case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0>(ma, mb, p, s);
     case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0>(ma, mb, p, s);
+    case ARMT_EPI_LSE:
+      if constexpr (BN == 256) return launch<BN, E_LSE, 0>(ma, mb, p, s);
+      break;
     case ARMT_EPI_SWIGLU:
       if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0>(ma, mb, p, s);
       break;
@@ -527,6 +568,8 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   p.c2_split = a.c2_split;
   p.ssq_out = a.ssq_out; p.ssq_in = a.ssq_in; p.ssq_stride = a.ssq_stride; p.ssq_np = a.ssq_np;
   p.norm_d = a.norm_d; p.norm_eps = a.norm_eps;
+  p.lse_part = reinterpret_cast<float2*>(a.lse_part); p.lse_ld = a.lse_ld; p.targets = a.targets;
+  p.lse_tgt = a.lse_tgt; p.lse_rows = a.lse_rows;
   p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
   p.swiglu_block = a.swiglu_block;

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) fold_phi_kernel(const __grid_constant__ A
 // (armt/memory.py:101-106,116-119 with z_i expanded over earlier tokens);
 // then coef_i, L_ij = coef_i K_ij (j < i), and z_M = z_0 + sum_i gamma_i phi_i.
 constexpr int QMAX = 8;  // M <= 256
-__global__ void __launch_bounds__(256) fold_chain_kernel(const __grid_constant__ ArmtMembers mem, float* __restrict__ z,
+__global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__ ArmtMembers mem, float* __restrict__ z,
                                                          __nv_bfloat16* __restrict__ memop, float eps, Geom q, Ws w) {
   extern __shared__ float sm[];
   const int Mp = q.Mp, M = q.M;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) fold_chain_kernel(const __grid_constant__
 #pragma unroll
         for (int v = 0; v < u; ++v) zq[u] = fmaf(gam[v], sK[(i0 + v) * Mp + i], zq[u]);
         const float nrm = i < M ? snrm[i] : 0.f;
-        gam[u] = (i < M && nrm > eps) ? 1.f - zq[u] / nrm : 0.f;
+        gam[u] = (i < M && nrm > eps) ? 1.f - __fdividef(zq[u], nrm) : 0.f;
       }
       if (lane < 4 && i0 + lane < M) {
         szq[i0 + lane] = lane == 0 ? zq[0] : lane == 1 ? zq[1] : lane == 2 ? zq[2] : zq[3];
@@ -270,63 +270,74 @@ __global__ void __launch_bounds__(256) fold_chain_kernel(const __grid_constant__
 // blocks: off-diagonal update from finished rows (L row block read as float4
 // broadcasts), then in-block forward substitution in registers. Output U^T as
 // the [hi | hi | lo] bf16x3 A operand of GEMM3.
+// Two columns per thread (n and n + 128): every LT broadcast load feeds 2x16 FMAs.
+constexpr int SOLVE_COLS = 256;
 __global__ void __launch_bounds__(128) fold_solve_kernel(const float* __restrict__ kvb, long long ld_kvb,
                                                          long long kvb_stride, int v_off, Geom q, Ws w) {
   extern __shared__ __align__(16) float sm[];
   const int Mp = q.Mp, M = q.M;
-  constexpr int US = 129;         // padded row: conflict-free column and row walks
-  float* LT = sm;                 // [Mp][Mp]: LT[j][i] = L_ij
-  float* us = LT + Mp * Mp;       // [Mp][US]
+  constexpr int US = SOLVE_COLS + 1;  // padded row: conflict-free column and row walks
+  float* LT = sm;                     // [Mp][Mp]: LT[j][i] = L_ij
+  float* us = LT + Mp * Mp;           // [Mp][US]
   const int g = blockIdx.y;
-  const int n0 = blockIdx.x * 128;
-  const int n = n0 + threadIdx.x;
-  const bool live = n < q.d;
+  const int n0 = blockIdx.x * SOLVE_COLS;
+  const int c0 = threadIdx.x, c1 = threadIdx.x + 128;
+  const bool live0 = n0 + c0 < q.d, live1 = n0 + c1 < q.d;
   const float4* Lg = reinterpret_cast<const float4*>(w.L + (long long)g * Mp * Mp);  // already LT layout
   for (int e = threadIdx.x; e < Mp * Mp / 4; e += blockDim.x) reinterpret_cast<float4*>(LT)[e] = Lg[e];
   const float* beta = w.beta + (long long)g * Mp;
   const float* coef = w.coef + (long long)g * Mp;
   const float* Pf = w.Pf + (long long)g * M * q.NP1;
   const float* kv = kvb + (long long)g * kvb_stride;
-  for (int i0 = 0; i0 < Mp; i0 += 16) {  // 32 independent loads in flight per thread
-    float vv[16], pv[16];
+  for (int i0 = 0; i0 < Mp; i0 += 8) {  // 32 independent loads in flight per thread
+    float v0[8], p0[8], v1[8], p1[8];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
+    for (int t = 0; t < 8; ++t) {
       const int i = i0 + t;
-      const bool ok = live && i < M;
-      vv[t] = ok ? kv[(long long)i * ld_kvb + v_off + n] : 0.f;
-      pv[t] = ok ? Pf[(long long)i * q.NP1 + n] : 0.f;
+      const bool ok = i < M;
+      v0[t] = (ok && live0) ? kv[(long long)i * ld_kvb + v_off + n0 + c0] : 0.f;
+      p0[t] = (ok && live0) ? Pf[(long long)i * q.NP1 + n0 + c0] : 0.f;
+      v1[t] = (ok && live1) ? kv[(long long)i * ld_kvb + v_off + n0 + c1] : 0.f;
+      p1[t] = (ok && live1) ? Pf[(long long)i * q.NP1 + n0 + c1] : 0.f;
     }
 #pragma unroll
-    for (int t = 0; t < 16; ++t) us[(i0 + t) * US + threadIdx.x] = beta[i0 + t] * vv[t] - coef[i0 + t] * pv[t];
+    for (int t = 0; t < 8; ++t) {
+      us[(i0 + t) * US + c0] = beta[i0 + t] * v0[t] - coef[i0 + t] * p0[t];
+      us[(i0 + t) * US + c1] = beta[i0 + t] * v1[t] - coef[i0 + t] * p1[t];
+    }
   }
   __syncthreads();
   for (int b = 0; b < Mp; b += 16) {
-    float x[16];
+    float x[16], y[16];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) x[t] = us[(b + t) * US + threadIdx.x];
+    for (int t = 0; t < 16; ++t) { x[t] = us[(b + t) * US + c0]; y[t] = us[(b + t) * US + c1]; }
     for (int j = 0; j < b; ++j) {
-      const float uj = us[j * US + threadIdx.x];
+      const float u0 = us[j * US + c0], u1 = us[j * US + c1];
       const float4* lrow = reinterpret_cast<const float4*>(LT + j * Mp + b);
 #pragma unroll
       for (int t4 = 0; t4 < 4; ++t4) {
         const float4 l = lrow[t4];
-        x[4 * t4 + 0] = fmaf(-l.x, uj, x[4 * t4 + 0]);
-        x[4 * t4 + 1] = fmaf(-l.y, uj, x[4 * t4 + 1]);
-        x[4 * t4 + 2] = fmaf(-l.z, uj, x[4 * t4 + 2]);
-        x[4 * t4 + 3] = fmaf(-l.w, uj, x[4 * t4 + 3]);
+        x[4 * t4 + 0] = fmaf(-l.x, u0, x[4 * t4 + 0]); y[4 * t4 + 0] = fmaf(-l.x, u1, y[4 * t4 + 0]);
+        x[4 * t4 + 1] = fmaf(-l.y, u0, x[4 * t4 + 1]); y[4 * t4 + 1] = fmaf(-l.y, u1, y[4 * t4 + 1]);
+        x[4 * t4 + 2] = fmaf(-l.z, u0, x[4 * t4 + 2]); y[4 * t4 + 2] = fmaf(-l.z, u1, y[4 * t4 + 2]);
+        x[4 * t4 + 3] = fmaf(-l.w, u0, x[4 * t4 + 3]); y[4 * t4 + 3] = fmaf(-l.w, u1, y[4 * t4 + 3]);
       }
     }
 #pragma unroll
     for (int t = 1; t < 16; ++t)
 #pragma unroll
-      for (int s = 0; s < t; ++s) x[t] = fmaf(-LT[(b + s) * Mp + b + t], x[s], x[t]);
+      for (int s = 0; s < t; ++s) {
+        const float l = LT[(b + s) * Mp + b + t];
+        x[t] = fmaf(-l, x[s], x[t]);
+        y[t] = fmaf(-l, y[s], y[t]);
+      }
 #pragma unroll
-    for (int t = 0; t < 16; ++t) us[(b + t) * US + threadIdx.x] = x[t];
+    for (int t = 0; t < 16; ++t) { us[(b + t) * US + c0] = x[t]; us[(b + t) * US + c1] = y[t]; }
   }
   __syncthreads();
   // U^T rows [hi | hi | lo]: warp w writes rows n0 + w, n0 + w + 4, ...; lanes walk tokens
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rr = warp; rr < 128; rr += 4) {
+  for (int rr = warp; rr < SOLVE_COLS; rr += 4) {
     if (n0 + rr >= q.d) break;
     __nv_bfloat16* out = w.UTs + ((long long)g * q.d + n0 + rr) * 3 * Mp;
     for (int i = 2 * lane; i < Mp; i += 64) {
@@ -395,13 +406,13 @@ extern "C" int armt_mem_fold_tc(const ArmtMembers* mem, const float* kvb, long l
   }
   const size_t chain_smem = sizeof(float) * ((size_t)q.Mp * q.Mp + 3 * (size_t)q.Mp);
   cudaFuncSetAttribute(fold_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem);
-  fold_chain_kernel<<<mem->G, 256, chain_smem, s>>>(*mem, z, mo, eps, q, w);
+  fold_chain_kernel<<<mem->G, 512, chain_smem, s>>>(*mem, z, mo, eps, q, w);
   ARMT_CHECK_LAUNCH("fold_chain");
 
-  const size_t solve_smem = sizeof(float) * ((size_t)q.Mp * q.Mp + (size_t)q.Mp * 129);
+  const size_t solve_smem = sizeof(float) * ((size_t)q.Mp * q.Mp + (size_t)q.Mp * (SOLVE_COLS + 1));
   ARMT_REQUIRE(solve_smem <= 227 * 1024, ARMT_ERR_UNSUPPORTED, "fold_tc: M too large for the solve");
   cudaFuncSetAttribute(fold_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem);
-  dim3 grid((d + 127) / 128, mem->G);
+  dim3 grid((d + SOLVE_COLS - 1) / SOLVE_COLS, mem->G);
   fold_solve_kernel<<<grid, 128, solve_smem, s>>>(kvb, ld_kvb, kvb_stride, v_off, q, w);
   ARMT_CHECK_LAUNCH("fold_solve");
 

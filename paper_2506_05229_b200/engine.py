@@ -516,6 +516,29 @@ class Engine:
         self.forward(slots, layers, stream)
         self.update(slots, layers, state, stream)
 
+    def unembed_lse(self, slot: int, ids: torch.Tensor, row0: int, n_tokens: int, part: torch.Tensor,
+                    tgt: torch.Tensor, stream: int) -> None:
+        """LM head with the fused next-token NLL epilogue: no logits are written;
+        per row and 256-wide vocab tile (max, sum exp) partials + the target logit."""
+        p, cfg = self.p, self.cfg
+        d, V, seg = cfg.d_model, cfg.vocab_size, cfg.segment_size
+        src = self.xs_bf if self.bf16 else self.xs
+        rows = max(0, min(seg, n_tokens - 1 - row0))
+        tiles = part.shape[1]
+
+        def fill(a):
+            a.M, a.N, a.K, a.ab_dtype = seg, V, d, p.ab
+            a.A, a.lda, a.a_stride = src.data_ptr(), d, p.T * d
+            a.B, a.ldb, a.b_stride = p.unemb.data_ptr(), d, V * d
+            a.C, a.ldc, a.c_stride, a.c_dtype = tgt.data_ptr(), 1, 0, F32  # unused by the LSE epilogue
+            a.epilogue = _lib.EPI_LSE
+            a.lse_part, a.lse_ld = part.data_ptr() + row0 * tiles * 8, tiles
+            a.targets = ids.data_ptr() + (row0 + 1) * 8
+            a.lse_tgt, a.lse_rows = tgt.data_ptr() + row0 * 4, rows
+            self._tables(a, [slot], [0], [0])
+        _lib.check(self.lib.armt_gemm(self._gemm(("lse", slot, part.data_ptr(), row0, rows), fill), stream),
+                   "unembed (fused nll)")
+
     def unembed(self, slot: int, out: torch.Tensor, row0: int, stream: int) -> None:
         """armt/layers.py:321-323: logits rows [row0, row0+seg) = xs[slot][:seg] @ U."""
         p, cfg = self.p, self.cfg

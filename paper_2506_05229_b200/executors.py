@@ -188,7 +188,7 @@ class Runner:
     launches) into one CUDA graph so replays pay no host launch overhead."""
 
     def __init__(self, prepared: PreparedWeights, plan: Plan, logits_dtype: torch.dtype | None = None,
-                 state_layers: int | None = None):
+                 state_layers: int | None = None, scoring_tokens: int | None = None):
         self.p = prepared
         self.plan = plan
         cfg = prepared.config
@@ -197,24 +197,22 @@ class Runner:
         dev = prepared.device
         seg = cfg.segment_size
         self.ids = torch.zeros(plan.n_segments * seg, dtype=torch.int64, device=dev)
-        if logits_dtype is None:
-            logits_dtype = torch.bfloat16 if prepared.dtype_name == "bf16" else torch.float32
-        self.logits = torch.empty(plan.n_segments * seg, cfg.vocab_size, dtype=logits_dtype, device=dev)
+        self.scoring_tokens = scoring_tokens
+        if scoring_tokens is not None:
+            # fused next-token NLL: no logits, only per-row/per-vocab-tile partials
+            if prepared.dtype_name != "bf16":
+                raise InputError("fused scoring runs on the bf16 tensor-core path")
+            n_tiles = -(-cfg.vocab_size // 256)
+            self.logits = None
+            self.lse_part = torch.empty(plan.n_segments * seg, n_tiles, 2, device=dev)
+            self.lse_tgt = torch.zeros(plan.n_segments * seg, device=dev)
+        else:
+            if logits_dtype is None:
+                logits_dtype = torch.bfloat16 if prepared.dtype_name == "bf16" else torch.float32
+            self.logits = torch.empty(plan.n_segments * seg, cfg.vocab_size, dtype=logits_dtype, device=dev)
         self.graph = None
         self.graph_state = None
         self.step_events = None
-
-    @property
-    def kernels_per_run(self) -> int:
-        n = 0
-        per_step = 10 if self.p.dtype_name == "bf16" else 12
-        for st in self.plan.steps:
-            if st.enter is not None:
-                n += 1
-            if st.nodes:
-                n += per_step + (1 if self.cfg.num_mem_tokens else -2) + 1
-            n += len(st.exits)
-        return n
 
     def _launch_all(self, state: MemoryState, stream: int, events=None) -> None:
         eng = self.engine
@@ -228,7 +226,10 @@ class Runner:
             if st.nodes:
                 eng.step(st.slots, st.layers, state, stream)
             for s, slot in st.exits:
-                eng.unembed(slot, self.logits, s * seg, stream)
+                if self.scoring_tokens is not None:
+                    eng.unembed_lse(slot, self.ids, s * seg, self.scoring_tokens, self.lse_part, self.lse_tgt, stream)
+                else:
+                    eng.unembed(slot, self.logits, s * seg, stream)
             if events is not None:
                 events[i][1].record()
 
@@ -368,7 +369,7 @@ class Session:
     """
 
     def __init__(self, prepared: PreparedWeights, n_tokens: int, schedule: str = "diagonal",
-                 graph: bool = True, shuffle_seed: int | None = None):
+                 graph: bool = True, shuffle_seed: int | None = None, scoring: bool = False):
         cfg = prepared.config
         self.p, self.cfg, self.n = prepared, cfg, int(n_tokens)
         S = -(-self.n // cfg.segment_size)
@@ -379,7 +380,8 @@ class Session:
         else:
             raise InputError(f"unknown schedule {schedule!r}")
         self.plan = plan
-        self.runner = Runner(prepared, plan)
+        self.scoring = scoring
+        self.runner = Runner(prepared, plan, scoring_tokens=self.n if scoring else None)
         self.state = MemoryState.fresh(cfg, prepared.device)
         self.nll_rows = torch.empty(max(self.n - 1, 1), device=prepared.device)
         self.use_graph = graph
@@ -426,12 +428,23 @@ class Session:
         else:
             self.state.A.zero_(); self.state.z.zero_()
             self.runner.run(self.state)
-        return self.runner.logits[:self.n]
+        return None if self.runner.logits is None else self.runner.logits[:self.n]
 
     def nll(self, tokens=None, targets: torch.Tensor | None = None) -> torch.Tensor:
         """Per-token next-token NLL (device, n-1 values); targets default to
-        the input ids shifted by one."""
+        the input ids shifted by one. A ``scoring=True`` session computes it in
+        the LM-head epilogue without materialising logits."""
         from . import _lib
+        if self.scoring:
+            if targets is not None:
+                raise InputError("a scoring session scores the next input token")
+            self.forward(tokens)
+            r = self.runner
+            _lib.check(_lib.load().armt_lse_finalize(r.lse_part.data_ptr(), r.lse_part.shape[1], r.lse_part.shape[1],
+                                                     r.lse_tgt.data_ptr(), r.ids.data_ptr() + 8,
+                                                     self.nll_rows.data_ptr(), self.n - 1,
+                                                     torch.cuda.current_stream().cuda_stream), "lse_finalize")
+            return self.nll_rows[:self.n - 1]
         logits = self.forward(tokens)
         if targets is None:
             targets = self.runner.ids[1:self.n]

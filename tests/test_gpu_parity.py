@@ -182,3 +182,25 @@ def test_store_then_retrieve_is_exact(dtype, key):
     assert np.array_equal(out[0, :5], values)
     out1 = assoc_retrieve(st, 1, act, prep).data.cpu().numpy()
     assert np.array_equal(out1[0, :5], np.zeros(5, np.float32))
+
+
+def test_fused_scoring_nll_matches_logits_path():
+    # LM-head epilogue NLL (no logits materialised) vs log-softmax of the logits
+    from paper_2506_05229_b200.executors import Session
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    prep = prepare_weights(conditioned_weights(cfg), "bf16")
+    n = 4 * cfg.segment_size - 5
+    tokens = torch.as_tensor(cli_tokens(cfg, n, seed=9)).cuda()
+    plain = Session(prep, n, graph=False)
+    logits = plain.forward(tokens).float()
+    want = -torch.log_softmax(logits[:-1].double(), -1).gather(1, tokens[1:, None])[:, 0]
+    via_kernel = plain.nll(tokens)
+    scoring = Session(prep, n, scoring=True)
+    got = scoring.nll(tokens)
+    assert scoring.runner.logits is None
+    assert float((via_kernel.double() - want).abs().max()) < 1e-3
+    # the fused path works from fp32 accumulators, the reference side from bf16-rounded
+    # logits (|logit| ~ 10 -> ~0.04 rounding): bound that difference, not equality
+    diff = (got.double() - want).abs()
+    assert float(diff.max()) < 0.05 and float(diff.mean()) < 5e-3
+    assert abs(float(got.double().mean() - want.mean())) < 2e-3
