@@ -37,7 +37,19 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 C2 = dict(n_layers=16, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024, num_mem_tokens=128,
           d_mem=64, vocab_size=128256)
+C5 = dict(n_layers=32, d_model=4096, n_heads=32, d_ff=14336, segment_size=1024, num_mem_tokens=128,
+          d_mem=64, vocab_size=128256)
 N_TOKENS = 131072
+# BASELINE.json configs as (model kwargs, tokens, description)
+CONFIGS = {
+    "c2": (C2, 131072, "C2: LLaMA-3.2-1B-shaped ARMT (L16 d2048 H32 ff8192), seg 1024, 128 mem tokens"),
+    "c3-512": (dict(C2, segment_size=512), 131072, "C3: C2 with segment 512"),
+    "c3-2048": (dict(C2, segment_size=2048), 131072, "C3: C2 with segment 2048"),
+    "c3-32k": (C2, 32768, "C3: C2 at 32,768 tokens"),
+    "c4": (C2, 1048576, "C4: C2 model, 1,048,576-token sequence"),
+    "c5": (C5, 131072, "C5: LLaMA-3.1-8B-shaped ARMT (L32 d4096 H32 ff14336), seg 1024, 128 mem tokens"),
+}
+EPS_C5 = 10000.0      # width 4096 needs a larger guard to stay finite over 128 segments (1000 diverges)
 EPS_ASSOC = 100.0     # SURVEY Appendix B conditioning: finite over all 128 C2 segments (scripts/c2_horizon.py)
 METRIC = "tokens/sec for one 131k-token seq, LLaMA-1B ARMT seg1024, 1/2/4/8 B200"
 
@@ -134,12 +146,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_weights(cfg):
-    """Reference initializer (armt/weights.py:98-138, seed 0), w_v_mem x 1/32."""
+def make_weights(cfg, init: str = "reference"):
+    """Reference initializer (armt/weights.py:98-138, seed 0), w_v_mem x 1/32.
+
+    ``init="device"`` draws the same distributions (N(0,1)/sqrt(fan_in), unit
+    gains) with torch's seeded generator on the GPU: the values differ from
+    the reference's PCG64 stream but the architecture/scales are identical;
+    used for the 8B-shaped config where a host f64 draw of 9.4 B parameters
+    would dominate the run.
+    """
     from dataclasses import replace
     from paper_2506_05229_b200 import init_weights
-    w = init_weights(cfg, dtype=np.float32)
-    return replace(w, w_v_mem=w.w_v_mem * np.float32(1.0 / 32))
+    from paper_2506_05229_b200.weights import GroupedWeights, expected_shapes
+    if init == "reference":
+        w = init_weights(cfg, dtype=np.float32)
+        return replace(w, w_v_mem=w.w_v_mem * np.float32(1.0 / 32))
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(cfg.seed)
+    shapes = expected_shapes(cfg)
+    fan = {"embedding": 1, "mem_embedding": 1, "w_out": cfg.d_ff}
+    arrays = {}
+    for name, shape in shapes.items():
+        if name in ("attn_gain", "mlp_gain"):
+            arrays[name] = torch.ones(shape, device="cuda")
+            continue
+        t = torch.randn(shape, generator=gen, device="cuda")
+        if name != "embedding" and name != "mem_embedding":
+            t *= 1.0 / np.sqrt(fan.get(name, cfg.d_model))
+        if name == "w_v_mem":
+            t *= 1.0 / 32
+        arrays[name] = t
+    return GroupedWeights(config=cfg, **arrays)
 
 
 def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: int = 16):
@@ -208,13 +245,19 @@ def device_arm(args, rank, world):
     from paper_2506_05229_b200.engine import prepare_weights
     from paper_2506_05229_b200.executors import Session
 
-    cfg = ModelConfig(**C2, eps_assoc=EPS_ASSOC, seed=0)
-    n = N_TOKENS if args.segments is None else args.segments * cfg.segment_size
+    model, n_cfg, desc = CONFIGS[args.config]
+    eps = args.eps if args.eps is not None else (EPS_C5 if args.config == "c5" else EPS_ASSOC)
+    cfg = ModelConfig(**model, eps_assoc=eps, seed=0)
+    n = args.tokens or n_cfg
+    if args.segments is not None:
+        n = args.segments * cfg.segment_size
     S = -(-n // cfg.segment_size)
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     t_setup = time.time()
-    w = make_weights(cfg)
+    init = args.init or ("device" if args.config == "c5" else "reference")
+    scoring_value = args.scoring or args.config == "c4"
+    w = make_weights(cfg, init)
     tokens = np.random.default_rng([0, n]).integers(0, cfg.vocab_size, n, dtype=np.int64)
 
     if world > 1:
@@ -222,7 +265,10 @@ def device_arm(args, rank, world):
         sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule)
     else:
         prep = prepare_weights(w, "bf16", dev)
-        sess = Session(prep, n, schedule=args.schedule)
+        if init == "device":
+            del w
+            torch.cuda.empty_cache()
+        sess = Session(prep, n, schedule=args.schedule, scoring=scoring_value)
     sess._load_ids(torch.as_tensor(tokens).to(dev))
 
     # roofline probe: events around every full-width gate/up GEMM, captured into the graph
@@ -281,7 +327,7 @@ def device_arm(args, rank, world):
     # Single GPU: a scoring Session fuses the next-token NLL into the LM-head epilogue
     # (no 33.6 GB logits round trip); the sharded path scores from the last rank's logits.
     launches_per_forward = sess.kernels_per_forward
-    if world == 1:
+    if world == 1 and not scoring_value:
         del sess
         torch.cuda.empty_cache()
         sess = Session(prep, n, schedule=args.schedule, scoring=True)
@@ -314,7 +360,7 @@ def device_arm(args, rank, world):
     mean_nll = float(host_nll.mean()) if rank == world - 1 else None
 
     peaks, peak_kind = load_peaks()
-    traffic = load_traffic()
+    traffic = load_traffic() if (args.config == "c2" and full_g == 16) else None
     d_ff_pad = sess.p.d_ff_pad
     gu_bytes = 2.0 * (full_g * cfg.tokens_per_segment * cfg.d_model + full_g * 2 * d_ff_pad * cfg.d_model
                       + full_g * cfg.tokens_per_segment * d_ff_pad)
@@ -329,7 +375,7 @@ def device_arm(args, rank, world):
     if rank != 0:
         return 0
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and init == "reference":
         r = cpu_oracle_rate(w, cfg, S)
         cpu = {"value": n / r["total_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
                "sample": f"{r['cells']} full-width C2 cells (retrieve+block+fold) + 1 segment LM head, numpy/BLAS "
@@ -338,9 +384,11 @@ def device_arm(args, rank, world):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic: reference seeded init (seed 0, w_v_mem/32, eps_assoc 100), cli token convention",
-        "config": {"workload": f"C2: LLaMA-3.2-1B-shaped ARMT (L16 d2048 H32 ff8192), seg 1024, 128 mem tokens, "
-                               f"{n} tokens", "schedule": args.schedule, "segments": S,
+        "data": (f"synthetic: reference seeded init (seed 0, w_v_mem/32, eps_assoc {eps:g}), cli token convention"
+                 if init == "reference" else
+                 f"synthetic: seeded device init with the reference's scales (w_v_mem/32, eps_assoc {eps:g}), cli tokens"),
+        "config": {"workload": f"{desc}, {n} tokens", "schedule": args.schedule, "segments": S,
+                   "init": init, "output": "fused NLL (no logits)" if scoring_value else "bf16 logits",
                    "parallelism": f"layer-shard{world}" if world > 1 else "single",
                    "l2": "inputs > L2 (3.3 GB bf16 weights, 33.6 GB logits); no flush",
                    "timing": "CUDA events around one CUDA-graph replay of the whole forward, max over ranks",
@@ -377,6 +425,12 @@ def main():
     ap.add_argument("--schedule", default="diagonal", choices=["diagonal", "sequential"])
     ap.add_argument("--segments", type=int, default=None, help="override S (profiling runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=None, help="override the sequence length")
+    ap.add_argument("--init", default=None, choices=["reference", "device"])
+    ap.add_argument("--eps", type=float, default=None, help="eps_assoc override (fixture conditioning)")
+    ap.add_argument("--scoring", action="store_true",
+                    help="time the fused-NLL forward (no logits) for the value too (implied for c4)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

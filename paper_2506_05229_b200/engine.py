@@ -111,7 +111,7 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
     cfg = weights.config
     resolve_dtype(dtype_name)
     for name, shape in expected_shapes(cfg).items():
-        got = np.shape(getattr(weights, name))
+        got = tuple(getattr(weights, name).shape)
         if tuple(got) != shape:
             raise InputError(f"weight tensor {name!r} has shape {got}, config expects {shape}")
     if not torch.cuda.is_available():
@@ -135,6 +135,8 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
     def up(name, sl=True):
         a = getattr(weights, name)
         a = a[lo:hi] if sl else a
+        if isinstance(a, torch.Tensor):
+            return a.to(dev, torch.float32).contiguous()
         return torch.as_tensor(np.ascontiguousarray(a)).to(dev, torch.float32)
 
     def kmajor(t):  # (L, in, out) -> (L, out, in)
