@@ -260,7 +260,7 @@ def device_arm(args, rank, world):
     w = make_weights(cfg, init)
     tokens = np.random.default_rng([0, n]).integers(0, cfg.vocab_size, n, dtype=np.int64)
 
-    if world > 1:
+    if world > 1 or args.force_sharded:
         from paper_2506_05229_b200.sharded import ShardedSession
         sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule)
     else:
@@ -327,7 +327,7 @@ def device_arm(args, rank, world):
     # Single GPU: a scoring Session fuses the next-token NLL into the LM-head epilogue
     # (no 33.6 GB logits round trip); the sharded path scores from the last rank's logits.
     launches_per_forward = sess.kernels_per_forward
-    if world == 1 and not scoring_value:
+    if world == 1 and not scoring_value and not args.force_sharded:
         del sess
         torch.cuda.empty_cache()
         sess = Session(prep, n, schedule=args.schedule, scoring=True)
@@ -429,6 +429,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=None, help="override the sequence length")
     ap.add_argument("--init", default=None, choices=["reference", "device"])
     ap.add_argument("--eps", type=float, default=None, help="eps_assoc override (fixture conditioning)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the layer-sharded session even at world size 1 (plumbing check)")
     ap.add_argument("--scoring", action="store_true",
                     help="time the fused-NLL forward (no logits) for the value too (implied for c4)")
     args = ap.parse_args()
@@ -436,14 +438,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl")
     try:
         return device_arm(args, rank, world)
     finally:
-        if world > 1:
+        if world > 1 or args.force_sharded:
             import torch
             torch.distributed.destroy_process_group()
 
