@@ -3,7 +3,8 @@
 // Reference: armt/layers.py:211-223 (scores = q k^T / sqrt(dh) + causal mask
 // over all T rows, max-subtracted softmax, ctx = P v, heads merged).
 //
-// One CTA = one 128-query tile of one (member, head); KV tiles of 128 keys.
+// Persistent CTAs (2 per SM for d_head 64) walk 128-query tiles of every
+// (member, head), heaviest first; KV tiles of 128 keys.
 //   warp 0      TMA: Q once, then K_j / V_j into a 2-stage ring (128B swizzle,
 //               read in place from the (T, 3d) QKV rows of the member)
 //   warp 1      MMA (one thread): S_j = Q K_j^T -> TMEM S[j%2] (M=128, N=128);
@@ -54,7 +55,7 @@ template <int DH> struct Cfg {
 struct Params {
   __nv_bfloat16* ctx;
   long long ld_ctx, ctx_stride;
-  int T, H, d, nq;
+  int T, H, G, d, nq;
   float scale_log2;
 };
 
@@ -79,18 +80,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ P
   uint64_t* p_empty = bar + 11;   // [2]
   uint64_t* o_full = bar + 13;    // [2]
   uint64_t* o_empty = bar + 15;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* q_empty = bar + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heaviest (last) query tiles first
-  const int qt = p.nq - 1 - (int)blockIdx.x;
-  const int h = blockIdx.y, g = blockIdx.z;
-  const int q0 = qt * BQ;
-  const int nkv = min(qt + 1, (p.T + BKV - 1) / BKV);
+  const int HG = p.H * p.G;
+  const int n_items = p.nq * HG;
+  const int n_kvmax = (p.T + BKV - 1) / BKV;
 
   if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
@@ -108,32 +109,49 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ P
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int colQ = h * DH, colK = p.d + h * DH, colV = 2 * p.d + h * DH;
+
+  // Persistent over work items (q-tile, head, member), heaviest q-tiles first.
+  // Every role walks the same item sequence; pipeline phases derive from the
+  // running KV-tile counter tt (and the item counter it for the Q buffer).
+  auto item = [&](int w, int& qt, int& h, int& g) {
+    qt = p.nq - 1 - w / HG;
+    const int rem = w - (w / HG) * HG;
+    h = rem % p.H;
+    g = rem / p.H;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int kb = 0; kb < KB; ++kb) tma_load_3d(sQ + kb * C::TILE, &tm, q_full, colQ + 64 * kb, q0, g);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], C::KV_BYTES);
-        uint8_t* base = sKV + st * C::KV_BYTES;
-        for (int kb = 0; kb < KB; ++kb) {
-          tma_load_3d(base + kb * C::TILE, &tm, &kv_full[st], colK + 64 * kb, j * BKV, g);
-          tma_load_3d(base + (KB + kb) * C::TILE, &tm, &kv_full[st], colV + 64 * kb, j * BKV, g);
+      int tt = 0, it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int qt, h, g;
+        item(w, qt, h, g);
+        const int nkv = min(qt + 1, n_kvmax);
+        const int colQ = h * DH, colK = p.d + h * DH, colV = 2 * p.d + h * DH;
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(q_full, C::Q_BYTES);
+        for (int kb = 0; kb < KB; ++kb) tma_load_3d(sQ + kb * C::TILE, &tm, q_full, colQ + 64 * kb, qt * BQ, g);
+        for (int j = 0; j < nkv; ++j) {
+          const int u = tt + j, st = u & 1;
+          mbar_wait(&kv_empty[st], ((u >> 1) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], C::KV_BYTES);
+          uint8_t* base = sKV + st * C::KV_BYTES;
+          for (int kb = 0; kb < KB; ++kb) {
+            tma_load_3d(base + kb * C::TILE, &tm, &kv_full[st], colK + 64 * kb, j * BKV, g);
+            tma_load_3d(base + (KB + kb) * C::TILE, &tm, &kv_full[st], colV + 64 * kb, j * BKV, g);
+          }
         }
+        tt += nkv;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idS = instr_desc<128, 128, 0>();
       constexpr uint32_t idO = instr_desc<128, DH, 1>();
-      mbar_wait(q_full, 0);
-      auto issue_pv = [&](int i) {
-        const int st = i & 1, pb = i % NP;
-        mbar_wait(&p_full[pb], (i / NP) & 1);
-        mbar_wait(&o_empty[st], ((i >> 1) & 1) ^ 1);
+      auto issue_pv = [&](int u) {
+        const int st = u & 1, pb = u % NP;
+        mbar_wait(&p_full[pb], (u / NP) & 1);
+        mbar_wait(&o_empty[st], ((u >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t pbase = smem_u32(sP + pb * C::P_BYTES);
         const uint32_t vbase = smem_u32(sKV + st * C::KV_BYTES + KB * C::TILE);
@@ -149,114 +167,147 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ P
         mma_commit(&kv_empty[st]);
         mma_commit(&p_empty[pb]);
       };
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1, sb = j % NS;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        mbar_wait(&s_empty[sb], ((j / NS) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t qbase = smem_u32(sQ);
-        const uint32_t kbase = smem_u32(sKV + st * C::KV_BYTES);
+      int tt = 0, it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int qt, h, g;
+        item(w, qt, h, g);
+        const int nkv = min(qt + 1, n_kvmax);
+        mbar_wait(q_full, it & 1);
+        for (int j = 0; j < nkv; ++j) {
+          const int u = tt + j, st = u & 1, sb = u % NS;
+          mbar_wait(&kv_full[st], (u >> 1) & 1);
+          mbar_wait(&s_empty[sb], ((u / NS) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t qbase = smem_u32(sQ);
+          const uint32_t kbase = smem_u32(sKV + st * C::KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < DH / 16; ++k)
-          mma_bf16(tmem + sb * 128, smem_desc_sw128(qbase + (k >> 2) * C::TILE) + 2 * (k & 3),
-                   smem_desc_sw128(kbase + (k >> 2) * C::TILE) + 2 * (k & 3), idS, k > 0);
-        mma_commit(&s_full[sb]);
-        if (j > 0) issue_pv(j - 1);
+          for (int k = 0; k < DH / 16; ++k)
+            mma_bf16(tmem + sb * 128, smem_desc_sw128(qbase + (k >> 2) * C::TILE) + 2 * (k & 3),
+                     smem_desc_sw128(kbase + (k >> 2) * C::TILE) + 2 * (k & 3), idS, k > 0);
+          mma_commit(&s_full[sb]);
+          if (j > 0) issue_pv(u - 1);
+        }
+        mma_commit(q_empty);  // every S MMA of this item has read Q
+        issue_pv(tt + nkv - 1);
+        tt += nkv;
       }
-      issue_pv(nkv - 1);
     }
   } else if (warp >= 4) {
     // ---------------- softmax: thread = query row r (TMEM lane)
     const int ew = warp & 3;
     const int r = ew * 32 + lane;
-    const int qrow = q0 + r;
     const uint32_t tl = tmem + ((uint32_t)(ew * 32) << 16);
     const float sl2 = p.scale_log2;
-    float o[DH];
+    int tt = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      int qt, h, g;
+      item(w, qt, h, g);
+      const int nkv = min(qt + 1, n_kvmax);
+      const int q0 = qt * BQ;
+      const int qrow = q0 + r;
+      float o[DH];
 #pragma unroll
-    for (int c = 0; c < DH; ++c) o[c] = 0.f;
-    float m = -INFINITY, l = 0.f, corr_prev = 1.f;
-    auto fold_o = [&](int i, float corr) {
-      const int st = i & 1;
-      mbar_wait(&o_full[st], (i >> 1) & 1);
-      tc_fence_after();
+      for (int c = 0; c < DH; ++c) o[c] = 0.f;
+      float m = -INFINITY, l = 0.f, corr_prev = 1.f;
+      auto fold_o = [&](int u, float corr) {
+        const int st = u & 1;
+        mbar_wait(&o_full[st], (u >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        float v[32];
-        __syncwarp();
-        tmem_ld32(tl + C::O_COL + st * DH + c0, v);
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tl + C::O_COL + st * DH + c0, v);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) o[c0 + c] = fmaf(o[c0 + c], corr, v[c]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[st]);
-    };
-    for (int j = 0; j < nkv; ++j) {
-      const int sb = j % NS, pb = j % NP;
-      const int k0 = j * BKV;
-      // valid keys of this row in the tile: c <= lim (causal and key < T); branch-free selects
-      const int lim = min(qrow, p.T - 1) - k0;
-      mbar_wait(&s_full[sb], (j / NS) & 1);
-      tc_fence_after();
-      // pass 1: row max
-      float mx = m;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        float v[32];
-        __syncwarp();
-        tmem_ld32(tl + sb * 128 + c0, v);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) mx = fmaxf(mx, (c0 + c <= lim) ? v[c] : -INFINITY);
-      }
-      const float corr = ex2((m - mx) * sl2);  // m = -inf on the first tile -> 0
-      m = mx;
-      const float nm = -mx * sl2;
-      if (j >= NP) mbar_wait(&p_empty[pb], ((j / NP) & 1) ^ 1);
-      // pass 2: p = exp2(s*sl2 - m*sl2), row sum, bf16 P row into the swizzled tile
-      float rs = 0.f;
-      uint8_t* prow = sP + pb * C::P_BYTES + r * 128;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        float v[32];
-        __syncwarp();
-        tmem_ld32(tl + sb * 128 + c0, v);
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float a = ex2(fmaf((c0 + c <= lim) ? v[c] : -INFINITY, sl2, nm));
-          const float b = ex2(fmaf((c0 + c + 1 <= lim) ? v[c + 1] : -INFINITY, sl2, nm));
-          rs += a + b;
-          pk[c >> 1] = pack_bf16x2(a, b);
+          for (int c = 0; c < 32; ++c) o[c0 + c] = fmaf(o[c0 + c], corr, v[c]);
         }
-        // keys c0..c0+31 = 4 chunks of 8 in sub-tile (c0 / 64), chunk index (c0 % 64) / 8 + u
-        uint8_t* sub = prow + (c0 >> 6) * C::TILE;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[st]);
+      };
+      for (int j = 0; j < nkv; ++j) {
+        const int u = tt + j, sb = u % NS, pb = u % NP;
+        const int k0 = j * BKV;
+        // valid keys of this row in the tile: c <= lim (causal and key < T)
+        const int lim = min(qrow, p.T - 1) - k0;
+        mbar_wait(&s_full[sb], (u / NS) & 1);
+        tc_fence_after();
+        // pass 1: row max (tree per 32-column chunk: no 128-long serial FMNMX chain)
+        const bool full = lim >= BKV - 1;  // warp-uniform for the tiles below the diagonal
+        float mx = m;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BKV; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tl + sb * 128 + c0, v);
+          if (!full) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = ((c0 & 63) >> 3) + u;
-          *reinterpret_cast<uint4*>(sub + ((chunk ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            for (int c = 0; c < 32; ++c) v[c] = (c0 + c <= lim) ? v[c] : -INFINITY;
+          }
+#pragma unroll
+          for (int w2 = 16; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int c = 0; c < w2; ++c) v[c] = fmaxf(v[c], v[c + w2]);
+          mx = fmaxf(mx, v[0]);
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      l = l * corr + rs;
-      fence_async_smem();  // make the generic-proxy P stores visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[pb]);
-      if (j > 0) fold_o(j - 1, corr_prev);
-      corr_prev = corr;
-    }
-    fold_o(nkv - 1, corr_prev);
-    if (qrow < p.T) {
-      const float inv = 1.f / l;
-      __nv_bfloat16* out = p.ctx + (long long)g * p.ctx_stride + (long long)qrow * p.ld_ctx + h * DH;
+        const float corr = ex2((m - mx) * sl2);  // m = -inf on the first tile -> 0
+        m = mx;
+        const float nm = -mx * sl2;
+        if (u >= NP) mbar_wait(&p_empty[pb], ((u / NP) & 1) ^ 1);
+        // pass 2: p = exp2(s*sl2 - m*sl2), row sum (tree), bf16 P row into the swizzled tile
+        float rs = 0.f;
+        uint8_t* prow = sP + pb * C::P_BYTES + r * 128;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BKV; c0 += 32) {
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tl + sb * 128 + c0, v);
+          if (!full) {
 #pragma unroll
-      for (int c = 0; c < DH; c += 8)
-        *reinterpret_cast<uint4*>(out + c) =
-            make_uint4(pack_bf16x2(o[c] * inv, o[c + 1] * inv), pack_bf16x2(o[c + 2] * inv, o[c + 3] * inv),
-                       pack_bf16x2(o[c + 4] * inv, o[c + 5] * inv), pack_bf16x2(o[c + 6] * inv, o[c + 7] * inv));
+            for (int c = 0; c < 32; ++c) v[c] = (c0 + c <= lim) ? v[c] : -INFINITY;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            v[c] = ex2(fmaf(v[c], sl2, nm));
+            v[c + 1] = ex2(fmaf(v[c + 1], sl2, nm));
+            pk[c >> 1] = pack_bf16x2(v[c], v[c + 1]);
+          }
+#pragma unroll
+          for (int w2 = 16; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int c = 0; c < w2; ++c) v[c] += v[c + w2];
+          rs += v[0];
+          // keys c0..c0+31 = 4 chunks of 8 in sub-tile (c0 / 64), chunk index (c0 % 64) / 8 + q
+          uint8_t* sub = prow + (c0 >> 6) * C::TILE;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = ((c0 & 63) >> 3) + q;
+            *reinterpret_cast<uint4*>(sub + ((chunk ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        l = l * corr + rs;
+        fence_async_smem();  // make the generic-proxy P stores visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
+        if (j > 0) fold_o(u - 1, corr_prev);
+        corr_prev = corr;
+      }
+      fold_o(tt + nkv - 1, corr_prev);
+      tt += nkv;
+      if (qrow < p.T) {
+        const float inv = 1.f / l;
+        __nv_bfloat16* out = p.ctx + (long long)g * p.ctx_stride + (long long)qrow * p.ld_ctx + h * DH;
+#pragma unroll
+        for (int c = 0; c < DH; c += 8)
+          *reinterpret_cast<uint4*>(out + c) =
+              make_uint4(pack_bf16x2(o[c] * inv, o[c + 1] * inv), pack_bf16x2(o[c + 2] * inv, o[c + 3] * inv),
+                         pack_bf16x2(o[c + 4] * inv, o[c + 5] * inv), pack_bf16x2(o[c + 6] * inv, o[c + 7] * inv));
+      }
     }
   }
   __syncwarp();
@@ -276,7 +327,7 @@ static int launch(int G, const void* qkv, long long ld_qkv, long long qkv_stride
   Params p;
   p.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
   p.ld_ctx = ld_ctx; p.ctx_stride = ctx_stride;
-  p.T = T; p.H = H; p.d = H * DH; p.nq = (T + BQ - 1) / BQ;
+  p.T = T; p.H = H; p.G = G; p.d = H * DH; p.nq = (T + BQ - 1) / BQ;
   p.scale_log2 = scale * 1.4426950408889634f;
   auto kern = attn_tc_kernel<DH>;
   static bool attr = false;
@@ -284,7 +335,10 @@ static int launch(int G, const void* qkv, long long ld_qkv, long long qkv_stride
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<DH>::SMEM);
     attr = true;
   }
-  kern<<<dim3(p.nq, H, G), NTHREADS, Cfg<DH>::SMEM, s>>>(tm, p);
+  const int items = p.nq * H * G;
+  const int per_sm = DH == 64 ? 2 : 1;
+  const int grid = items < per_sm * num_sms() ? items : per_sm * num_sms();
+  kern<<<grid, NTHREADS, Cfg<DH>::SMEM, s>>>(tm, p);
   ARMT_CHECK_LAUNCH("attention tcgen05");
   return ARMT_OK;
 }
