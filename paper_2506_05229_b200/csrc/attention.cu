@@ -315,6 +315,8 @@ static int launch_bf16(int G, const void* qkv, long long ld_qkv, long long qkv_s
 }  // namespace armt
 
 namespace armt {
+int attention_pp(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx, long long ld_ctx,
+                 long long ctx_stride, int T, int H, float scale, cudaStream_t s);
 int attention_tc(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx, long long ld_ctx,
                  long long ctx_stride, int T, int H, int dh, float scale, cudaStream_t s);
 }
@@ -339,12 +341,16 @@ extern "C" int armt_attention(int G, const void* qkv, long long ld_qkv, long lon
   }
   ARMT_REQUIRE(dh % 8 == 0 && ld_qkv % 8 == 0 && ld_ctx % 2 == 0, ARMT_ERR_DIM,
                "attention bf16: head dim and row strides must be multiples of 8");
-  // tcgen05 kernel for d_head 64/128 (ARMT_ATTN=mma forces the mma.sync kernel for A/B runs)
-  static const bool force_mma = [] {
+  // tcgen05 kernels: ping-pong pairs for d_head 64, one tile per CTA for 128
+  // (ARMT_ATTN=mma forces the mma.sync kernel, ARMT_ATTN=tc the single-tile
+  // tcgen05 kernel at d_head 64, for A/B runs)
+  static const char force = [] {
     const char* e = getenv("ARMT_ATTN");
-    return e != nullptr && e[0] == 'm';
+    return e != nullptr ? e[0] : '\0';
   }();
-  if ((dh == 64 || dh == 128) && !force_mma)
+  if (dh == 64 && force != 'm' && force != 't')
+    return attention_pp(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, scale, s);
+  if ((dh == 64 || dh == 128) && force != 'm')
     return attention_tc(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 16) return launch_bf16<16>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 32) return launch_bf16<32>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);

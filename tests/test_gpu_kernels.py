@@ -190,6 +190,23 @@ def test_attention_matches_reference(dtype, T, H, dh):
     assert rel(ctx.float(), want) < (1e-2 if dtype == "bf16" else 1e-6)
 
 
+@pytest.mark.parametrize("T", [64, 256, 300, 1152])
+@pytest.mark.parametrize("amp", [1.0, 6.0])
+def test_attention_dh64_pairs_and_lazy_rescale(T, amp):
+    # d_head 64 runs the ping-pong kernel: odd / even / single query-tile counts,
+    # a ragged tail, and large scores (amp 6 -> score spread ~ 36 / 8 per row)
+    # that force the lazy running-max raises and O rescales in TMEM
+    torch.manual_seed(7)
+    G, H, dh = 3, 2, 64
+    d = H * dh
+    qkv = (amp * torch.randn(G, T, 3 * d, device=DEV)).to(torch.bfloat16)
+    ctx = torch.zeros(G, T, d, device=DEV, dtype=torch.bfloat16)
+    _lib.check(LIB.armt_attention(G, qkv.data_ptr(), 3 * d, T * 3 * d, ctx.data_ptr(), d, T * d, BF16, T, H, dh,
+                                  1.0 / math.sqrt(dh), stream()), "attention")
+    want = attention_ref(qkv.float(), H, dh)
+    assert rel(ctx.float(), want) < 1e-2
+
+
 def test_dpfp_known_answers_on_device():
     # pkg/tests/test_memory.py:25-33 pinned on the device feature map
     from paper_2506_05229_b200.layers import dpfp
