@@ -87,6 +87,8 @@ typedef struct {
   const float* rope_cos; const float* rope_sin;  /* ROPE: (head_dim/2, M) tables, position-contiguous */
   int head_dim; int rope_cols;
   int swiglu_block;                     /* SWIGLU: cols [t*2b, t*2b+b) gate, [t*2b+b, (t+1)*2b) up */
+  int max_ctas;                         /* bf16 engine: cap on resident CTAs (0 = one per SM); lets a
+                                           launch leave SMs free for a concurrent stream */
   int a_slot[ARMT_MAX_MEMBERS];
   int b_index[ARMT_MAX_MEMBERS];
   int c_slot[ARMT_MAX_MEMBERS];

@@ -56,6 +56,7 @@ class ArmtGemmArgs(ctypes.Structure):
         ("rope_cos", _P), ("rope_sin", _P),
         ("head_dim", _I), ("rope_cols", _I),
         ("swiglu_block", _I),
+        ("max_ctas", _I),
         ("a_slot", _I * MAX_MEMBERS),
         ("b_index", _I * MAX_MEMBERS),
         ("c_slot", _I * MAX_MEMBERS),

@@ -50,6 +50,7 @@ struct Params {
   float eps;
   const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
   int swiglu_block;
+  int max_ctas;
   short a_slot[ARMT_MAX_MEMBERS];
   short b_index[ARMT_MAX_MEMBERS];
   short c_slot[ARMT_MAX_MEMBERS];
@@ -470,7 +471,8 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM_BYTES);
     attr_done = true;
   }
-  const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+  const int cap = p.max_ctas > 0 && p.max_ctas < num_sms() ? p.max_ctas : num_sms();
+  const int grid = p.num_tiles < cap ? p.num_tiles : cap;
   kern<<<grid, NUM_THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ma, mb, p);
   ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
   return ARMT_OK;
@@ -573,6 +575,7 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
   p.swiglu_block = a.swiglu_block;
+  p.max_ctas = a.max_ctas;
   for (int g = 0; g < a.G; ++g) {
     p.a_slot[g] = (short)a.a_slot[g];
     p.b_index[g] = (short)a.b_index[g];

@@ -519,7 +519,7 @@ class Engine:
         self.update(slots, layers, state, stream)
 
     def unembed_lse(self, slot: int, ids: torch.Tensor, row0: int, n_tokens: int, part: torch.Tensor,
-                    tgt: torch.Tensor, stream: int) -> None:
+                    tgt: torch.Tensor, stream: int, max_ctas: int = 0) -> None:
         """LM head with the fused next-token NLL epilogue: no logits are written;
         per row and 256-wide vocab tile (max, sum exp) partials + the target logit."""
         p, cfg = self.p, self.cfg
@@ -537,11 +537,12 @@ class Engine:
             a.lse_part, a.lse_ld = part.data_ptr() + row0 * tiles * 8, tiles
             a.targets = ids.data_ptr() + (row0 + 1) * 8
             a.lse_tgt, a.lse_rows = tgt.data_ptr() + row0 * 4, rows
+            a.max_ctas = max_ctas
             self._tables(a, [slot], [0], [0])
-        _lib.check(self.lib.armt_gemm(self._gemm(("lse", slot, part.data_ptr(), row0, rows), fill), stream),
+        _lib.check(self.lib.armt_gemm(self._gemm(("lse", slot, part.data_ptr(), row0, rows, max_ctas), fill), stream),
                    "unembed (fused nll)")
 
-    def unembed(self, slot: int, out: torch.Tensor, row0: int, stream: int) -> None:
+    def unembed(self, slot: int, out: torch.Tensor, row0: int, stream: int, max_ctas: int = 0) -> None:
         """armt/layers.py:321-323: logits rows [row0, row0+seg) = xs[slot][:seg] @ U."""
         p, cfg = self.p, self.cfg
         d, V, seg = cfg.d_model, cfg.vocab_size, cfg.segment_size
@@ -554,5 +555,7 @@ class Engine:
             a.B, a.ldb, a.b_stride = p.unemb.data_ptr(), d, V * d
             a.C, a.ldc, a.c_stride, a.c_dtype = out.data_ptr() + row0 * V * out.element_size(), V, seg * V, odt
             a.epilogue = EPI_STORE
+            a.max_ctas = max_ctas
             self._tables(a, [slot], [0], [0])
-        _lib.check(self.lib.armt_gemm(self._gemm(("lm", slot, out.data_ptr(), row0), fill), stream), "unembed")
+        _lib.check(self.lib.armt_gemm(self._gemm(("lm", slot, out.data_ptr(), row0, max_ctas), fill), stream),
+                   "unembed")

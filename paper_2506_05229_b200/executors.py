@@ -127,13 +127,18 @@ class Plan:
 
 
 def sequential_plan(n_segments: int, n_layers: int) -> Plan:
-    """armt/executors.py:134-147: one node per step, row-major (s, l)."""
+    """armt/executors.py:134-147: one node per step, row-major (s, l).
+
+    Two activation slots alternate between consecutive segments so that a
+    segment's LM head (side stream) can overlap the next segment's steps."""
     steps = []
+    n_slots = min(n_segments, 2)
     for s in range(n_segments):
+        k = s % n_slots
         for l in range(n_layers):
-            steps.append(Step([Node(s, l)], [0], [l], (s, 0) if l == 0 else None,
-                              [(s, 0)] if l == n_layers - 1 else []))
-    return Plan("sequential", n_segments, n_layers, 1, steps)
+            steps.append(Step([Node(s, l)], [k], [l], (s, k) if l == 0 else None,
+                              [(s, k)] if l == n_layers - 1 else []))
+    return Plan("sequential", n_segments, n_layers, n_slots, steps)
 
 
 def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = None,
@@ -148,7 +153,9 @@ def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = Non
     (empty) so step indices stay global.
     """
     S, L = n_segments, n_layers
-    n_slots = min(S, L)
+    # one slot more than the in-flight maximum: the exiting segment's slot is
+    # not re-embedded on the next step, so its LM head can overlap that step
+    n_slots = min(S, L + 1)
     rng = None if shuffle_seed is None else np.random.default_rng(shuffle_seed)
     flying: list[list[int]] = []   # [segment, cursor]
     nxt = 0
@@ -176,6 +183,12 @@ def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = Non
             m[1] += 1
         flying = [m for m in flying if m[1] < L]
     return Plan("diagonal", S, L, n_slots, steps)
+
+
+# SMs left to the main stream while an LM head runs beside it (the fold's
+# latency-bound kernels, the next step's small launches)
+LM_FREE_SMS = int(__import__("os").environ.get("ARMT_LM_FREE_SMS", "16"))
+LM_OVERLAP = __import__("os").environ.get("ARMT_LM_OVERLAP", "0") == "1"
 
 
 # =========================================================================
@@ -213,25 +226,56 @@ class Runner:
         self.graph = None
         self.graph_state = None
         self.step_events = None
+        # LM head on a side stream (bf16 engine): it leaves SMs to the memory update
+        from . import _lib
+        self.lm_overlap = prepared.dtype_name == "bf16" and LM_OVERLAP
+        self.lm_ctas = max(1, int(_lib.load().armt_num_sms()) - LM_FREE_SMS)
+        self.side = torch.cuda.Stream(device=dev) if self.lm_overlap else None
 
     def _launch_all(self, state: MemoryState, stream: int, events=None) -> None:
+        """Issue every step. The LM head of an exiting segment runs on a side
+        stream with ``lm_ctas`` CTAs, overlapping the memory update of its
+        step and the following step(s) on the SMs it leaves free; the main
+        stream waits for it only before that segment's slot is re-embedded."""
         eng = self.engine
         seg = self.cfg.segment_size
+        cur = torch.cuda.ExternalStream(stream, device=self.p.device)
+        overlap = self.lm_overlap and events is None
+        pending: dict[int, torch.cuda.Event] = {}   # slot -> LM head done
         for i, st in enumerate(self.plan.steps):
             if events is not None:
                 events[i][0].record()
             if st.enter is not None:
                 s, slot = st.enter
+                if slot in pending:
+                    cur.wait_event(pending.pop(slot))
                 eng.embed(self.ids[s * seg:(s + 1) * seg], slot, stream)
             if st.nodes:
-                eng.step(st.slots, st.layers, state, stream)
+                eng.retrieve(st.slots, st.layers, state, stream)
+                eng.forward(st.slots, st.layers, stream)
+            lm_stream, ctas = stream, 0
+            if st.exits and overlap:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self.side.wait_event(ev)
+                lm_stream, ctas = self.side.cuda_stream, self.lm_ctas
             for s, slot in st.exits:
                 if self.scoring_tokens is not None:
-                    eng.unembed_lse(slot, self.ids, s * seg, self.scoring_tokens, self.lse_part, self.lse_tgt, stream)
+                    eng.unembed_lse(slot, self.ids, s * seg, self.scoring_tokens, self.lse_part, self.lse_tgt,
+                                    lm_stream, ctas)
                 else:
-                    eng.unembed(slot, self.logits, s * seg, stream)
+                    eng.unembed(slot, self.logits, s * seg, lm_stream, ctas)
+            if st.exits and overlap:
+                done = torch.cuda.Event()
+                done.record(self.side)
+                for s, slot in st.exits:
+                    pending[slot] = done
+            if st.nodes:
+                eng.update(st.slots, st.layers, state, stream)
             if events is not None:
                 events[i][1].record()
+        for ev in pending.values():
+            cur.wait_event(ev)
 
     def run(self, state: MemoryState, timed: bool = False) -> None:
         """Eager replay on the current stream (state mutated in place)."""

@@ -57,8 +57,18 @@ def gemm(G, Mr, N, K, epi=_lib.EPI_STORE, c_dtype=BF16, **kw):
     a.C, a.ldc, a.c_stride, a.c_dtype = C.data_ptr(), ncol, Mr * ncol, c_dtype
     a.epilogue = epi
     keep = [A, B, C]
-    if epi in (_lib.EPI_RESIDUAL,):
+    if epi in (_lib.EPI_RESIDUAL, _lib.EPI_RETRIEVE):
+        # as in the step: in-place f32 stream + bf16 copy + per-64-column sum-of-squares partials
         a.R, a.ldr, a.r_stride = C.data_ptr(), ncol, Mr * ncol
+        C2 = torch.zeros(G, Mr, ncol, device="cuda", dtype=torch.bfloat16)
+        ssq = torch.zeros(G, Mr, (ncol + 63) // 64, device="cuda")
+        a.C2, a.ldc2, a.c2_stride = C2.data_ptr(), ncol, Mr * ncol
+        a.ssq_out, a.ssq_stride, a.ssq_np = ssq.data_ptr(), Mr * ssq.shape[2], ssq.shape[2]
+        keep += [C2, ssq]
+    if epi == _lib.EPI_RETRIEVE:
+        den = torch.ones(G, Mr, device="cuda")
+        a.den, a.den_stride, a.eps = den.data_ptr(), Mr, 1e-6
+        keep.append(den)
     if epi == _lib.EPI_SWIGLU:
         a.swiglu_block = 128
     if epi == _lib.EPI_ROPE:
@@ -81,14 +91,29 @@ def main():
     ap.add_argument("--G", type=int, default=16)
     ap.add_argument("--ops", default="gu,down,qkv,o,kvb,num,attn,fold,foldtc,lm")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--flags", default=None, help="A/B: comma list of ARMT_GEMM_FLAGS values, interleaved")
+    ap.add_argument("--repeat", type=int, default=1)
     args = ap.parse_args()
+    if args.flags:
+        for rep in range(args.repeat):
+            for fl in args.flags.split(","):
+                os.environ["ARMT_GEMM_FLAGS"] = fl
+                for op in args.ops.split(","):
+                    spec = {"down": (G_ := args.G, T, d, F, _lib.EPI_RESIDUAL, F32),
+                            "o": (G_, T, d, d, _lib.EPI_RESIDUAL, F32),
+                            "num": (G_, T, d, 384, _lib.EPI_RETRIEVE, F32)}[op]
+                    fn, flops, keep = gemm(*spec)
+                    us = timeit(fn, args.iters)
+                    print(json.dumps({"op": op, "flags": fl, "rep": rep, "us": round(us, 1)}), flush=True)
+                    del keep
+        return
     G = args.G
     pk = peaks()
     for op in args.ops.split(","):
         if op in ("gu", "down", "qkv", "o", "kvb", "num", "lm"):
             spec = {"gu": (G, T, 2 * F, d, _lib.EPI_SWIGLU, BF16), "down": (G, T, d, F, _lib.EPI_RESIDUAL, F32),
                     "qkv": (G, T, 3 * d, d, _lib.EPI_ROPE, BF16), "o": (G, T, d, d, _lib.EPI_RESIDUAL, F32),
-                    "kvb": (G, M, 2128, d, _lib.EPI_STORE, F32), "num": (G, T, d, 384, _lib.EPI_STORE, F32),
+                    "kvb": (G, M, 2128, d, _lib.EPI_STORE, F32), "num": (G, T, d, 384, _lib.EPI_RETRIEVE, F32),
                     "lm": (1, 1024, V, d, _lib.EPI_STORE, BF16)}[op]
             fn, flops, keep = gemm(*spec)
             us = timeit(fn, args.iters)
