@@ -27,6 +27,8 @@
 #include <cudaTypedefs.h>
 #include <vector>
 #include <mutex>
+#include <cstdlib>
+#include <cstring>
 
 #include "tc_ptx.cuh"
 
@@ -48,18 +50,25 @@ struct Params {
   float2* lse_part; long long lse_ld; const long long* targets; float* lse_tgt; int lse_rows;
   const float* den; long long den_stride;
   float eps;
-  const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols;
+  const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols; int rope_ld;
   int swiglu_block;
   int max_ctas;
+  int pf, pf_a;  // L2 prefetch distance in k-blocks for B (and A) tiles; 0 = off
+  int row0;    // first row of every member this launch covers (rows [row0, M))
+  int prof;    // ARMT_GEMM_PROF=1: accumulate wait cycles of the producer / MMA issuer
   short a_slot[ARMT_MAX_MEMBERS];
   short b_index[ARMT_MAX_MEMBERS];
   short c_slot[ARMT_MAX_MEMBERS];
 };
 
-template <int BN> struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+// PAIR: a 2-CTA cluster computes a 256 x BN tile with one cta_group::2 MMA per K
+// step; each CTA holds its 128 A rows and half (BN/2) of the B rows, so per-CTA
+// operand traffic per flop drops by a third and 6 stages fit in the same smem.
+template <int BN, bool PAIR = false> struct Cfg {
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
+  static constexpr int STAGES = PAIR ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
@@ -140,11 +149,17 @@ __device__ __forceinline__ void rope_chunk(float (&x)[CH], const float* cos_col,
 }
 
 // ---------------------------------------------------------------- kernel
-template <int BN, int EPI, int DH>
+// [0] MMA: cycles waiting for a full stage, [1] MMA: waiting for a free accumulator,
+// [2] MMA: total cycles in the tile loop, [3] producer: waiting for an empty stage,
+// [4] tiles, [5] epilogue: cycles waiting for a full accumulator, [6] epilogue: total
+__device__ unsigned long long g_gemm_prof[8];
+
+template <int BN, int EPI, int DH, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ Params p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, PAIR>;
+  constexpr int TM = PAIR ? 2 * BM : BM;   // rows per tile (per pair)
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -159,6 +174,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -166,16 +184,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], PAIR ? 8 : 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tmem_slot)), "r"(C::TMEM_COLS) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(C::TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(tmem_slot)), "r"(C::TMEM_COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -185,42 +210,87 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) {
       // ---------------- TMA producer
       int stage = 0; uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      unsigned long long w_empty = 0;
+      for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
         const int g = tile / tiles_mn, r = tile - g * tiles_mn;
         const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
         const int a_slot = p.a_slot[g], b_idx = p.b_index[g];
+        const int a_row = p.row0 + mb * TM + (int)rank * BM;
+        const int b_row = nb * BN + (int)rank * C::B_ROWS;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
+          if (p.prof) {
+            const long long t0 = clock64();
+            mbar_wait(&empty[stage], phase ^ 1);
+            w_empty += clock64() - t0;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM, a_slot);
-          tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN, b_idx);
+          if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's full barrier; the leader arms it
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            const uint32_t lbar = mapa_shared(&full[stage], 0);
+            tma_load_3d_pair(sA + stage * C::A_BYTES, &tmA, lbar, kb * BK, a_row, a_slot);
+            tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, lbar, kb * BK, b_row, b_idx);
+          } else {
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
+            tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, b_row, b_idx);
+          }
+          if (p.pf > 0 && kb + p.pf < p.k_blocks) {
+            // warm L2 with the operand tiles p.pf k-blocks ahead (weights miss to HBM)
+            tma_prefetch_3d(&tmB, (kb + p.pf) * BK, b_row, b_idx);
+            if (p.pf_a) tma_prefetch_3d(&tmA, (kb + p.pf) * BK, a_row, a_slot);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (p.prof) atomicAdd(&g_gemm_prof[3], w_empty);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
-      constexpr uint32_t idesc = instr_desc<BM, BN>();
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (single thread; the pair leader in PAIR mode)
+      constexpr uint32_t idesc = instr_desc<TM, BN>();
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      unsigned long long w_full = 0, w_acc = 0, n_tiles = 0;
+      const long long t_start = clock64();
+      for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+        if (p.prof) {
+          const long long t0 = clock64();
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          w_acc += clock64() - t0;
+          ++n_tiles;
+        }
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
+          if (p.prof) {
+            const long long t0 = clock64();
+            mbar_wait(&full[stage], phase);
+            w_full += clock64() - t0;
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t a_desc = smem_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t b_desc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-            mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the swizzle atom
+            if constexpr (PAIR) mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+            else mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (PAIR) mma_commit_pair(&empty[stage]);
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
+        else mma_commit(&tfull[acc]);
         acc ^= 1; if (acc == 0) acc_phase ^= 1;
+      }
+      if (p.prof) {
+        atomicAdd(&g_gemm_prof[0], w_full);
+        atomicAdd(&g_gemm_prof[1], w_acc);
+        atomicAdd(&g_gemm_prof[2], (unsigned long long)(clock64() - t_start));
+        atomicAdd(&g_gemm_prof[4], n_tiles);
       }
     }
   } else if (warp >= 4) {
@@ -229,12 +299,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int eg = (warp - 4) >> 2;
     const int acc = eg;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x + eg * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x) {
+    for (int tile = tile0 + eg * tstep; tile < p.num_tiles; tile += 2 * tstep) {
       const int g = tile / tiles_mn, r = tile - g * tiles_mn;
       const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
-      const int row = mb * BM + ew * 32 + lane;
+      const int row = p.row0 + mb * TM + (int)rank * BM + ew * 32 + lane;
       const bool live = row < p.M;
       const int c_slot = p.c_slot[g];
+      if (p.prof && lane == 0) {
+        const long long t0 = clock64();
+        mbar_wait(&tfull[acc], acc_phase);
+        atomicAdd(&g_gemm_prof[5], (unsigned long long)(clock64() - t0));
+      }
+      __syncwarp();
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
@@ -333,7 +409,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 if (rot) {
 #pragma unroll
                   for (int j = 0; j < 32; ++j) {
-                    const float cs = cos_col[(long long)(32 * q + j) * p.M], sn = sin_col[(long long)(32 * q + j) * p.M];
+                    const float cs = cos_col[(long long)(32 * q + j) * p.rope_ld], sn = sin_col[(long long)(32 * q + j) * p.rope_ld];
                     const float a = x1[j], b = x2[j];
                     x1[j] = a * cs - b * sn;
                     x2[j] = b * cs + a * sn;
@@ -350,7 +426,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if (live && n0 < p.N) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) x[j] *= rs;
-              if (rot) rope_chunk<DH, 32>(x, cos_col, sin_col, p.M);
+              if (rot) rope_chunk<DH, 32>(x, cos_col, sin_col, p.rope_ld);
               store_row32(p.C, ARMT_BF16, off, n0, p.N, p.ldc, x);
             }
           }
@@ -414,7 +490,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_remote(mapa_shared(&tempty[acc], 0));  // leader's barrier
+        else mbar_arrive(&tempty[acc]);
+      }
       acc_phase ^= 1;
     }
   }
@@ -422,10 +501,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer may still read our smem / signal our barriers
   tc_fence_after();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(C::TMEM_COLS) : "memory");
+  if (warp == 2) {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(C::TMEM_COLS) : "memory");
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -463,17 +548,41 @@ static int make_map(CUtensorMap* map, const void* base, long long cols, long lon
   return ARMT_OK;
 }
 
-template <int BN, int EPI, int DH>
+template <int BN, int EPI, int DH, bool PAIR>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
-  auto kern = gemm_kernel<BN, EPI, DH>;
+  auto kern = gemm_kernel<BN, EPI, DH, PAIR>;
+  constexpr int smem = Cfg<BN, PAIR>::SMEM_BYTES;
+  static_assert(smem <= 227 * 1024, "GEMM shared memory budget");
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM_BYTES);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (PAIR) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr_done = true;
   }
   const int cap = p.max_ctas > 0 && p.max_ctas < num_sms() ? p.max_ctas : num_sms();
-  const int grid = p.num_tiles < cap ? p.num_tiles : cap;
-  kern<<<grid, NUM_THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ma, mb, p);
+  if constexpr (PAIR) {
+    // one 2-CTA cluster per pair of SMs, persistent over pair tiles
+    const int pairs = cap / 2 < 1 ? 1 : cap / 2;
+    const int grid = 2 * (p.num_tiles < pairs ? p.num_tiles : pairs);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
+    ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 pair gemm launch: %s", cudaGetErrorString(e));
+  } else {
+    const int grid = p.num_tiles < cap ? p.num_tiles : cap;
+    kern<<<grid, NUM_THREADS, smem, s>>>(ma, mb, p);
+  }
   ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
   return ARMT_OK;
 }
@@ -481,6 +590,11 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
 static int pick_bn(const ArmtGemmArgs& a) {
   if (a.epilogue == ARMT_EPI_SWIGLU) return 2 * a.swiglu_block;
   if (a.epilogue == ARMT_EPI_LSE) return 256;  // lse_ld = ceil(N / 256) partials per row
+  if (const char* f = getenv("ARMT_GEMM_BN")) {  // tests: force a tile width
+    const int v = atoi(f);
+    if ((v == 64 || v == 128 || v == 256) && (a.epilogue != ARMT_EPI_ROPE || (v >= 128 && v % a.head_dim == 0)))
+      return v;
+  }
   const int sms = num_sms();
   const long long tm = (a.M + BM - 1) / BM;
   const bool rope = a.epilogue == ARMT_EPI_ROPE;
@@ -500,27 +614,27 @@ static int pick_bn(const ArmtGemmArgs& a) {
   return best;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 static int dispatch_epi(const ArmtGemmArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
                         cudaStream_t s) {
   switch (a.epilogue) {
-    case ARMT_EPI_STORE: return launch<BN, E_STORE, 0>(ma, mb, p, s);
-    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0>(ma, mb, p, s);
-    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0>(ma, mb, p, s);
+    case ARMT_EPI_STORE: return launch<BN, E_STORE, 0, PAIR>(ma, mb, p, s);
+    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0, PAIR>(ma, mb, p, s);
+    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0, PAIR>(ma, mb, p, s);
     case ARMT_EPI_LSE:
-      if constexpr (BN == 256) return launch<BN, E_LSE, 0>(ma, mb, p, s);
+      if constexpr (BN == 256) return launch<BN, E_LSE, 0, PAIR>(ma, mb, p, s);
       break;
     case ARMT_EPI_SWIGLU:
-      if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0>(ma, mb, p, s);
+      if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0, PAIR>(ma, mb, p, s);
       break;
     case ARMT_EPI_ROPE:
       if constexpr (BN >= 128) {
         switch (a.head_dim) {
-          case 8: return launch<BN, E_ROPE, 8>(ma, mb, p, s);
-          case 16: return launch<BN, E_ROPE, 16>(ma, mb, p, s);
-          case 32: return launch<BN, E_ROPE, 32>(ma, mb, p, s);
-          case 64: return launch<BN, E_ROPE, 64>(ma, mb, p, s);
-          case 128: return launch<BN, E_ROPE, 128>(ma, mb, p, s);
+          case 8: return launch<BN, E_ROPE, 8, PAIR>(ma, mb, p, s);
+          case 16: return launch<BN, E_ROPE, 16, PAIR>(ma, mb, p, s);
+          case 32: return launch<BN, E_ROPE, 32, PAIR>(ma, mb, p, s);
+          case 64: return launch<BN, E_ROPE, 64, PAIR>(ma, mb, p, s);
+          case 128: return launch<BN, E_ROPE, 128, PAIR>(ma, mb, p, s);
           default: break;
         }
       }
@@ -537,14 +651,9 @@ int make_tma_map_bf16(CUtensorMap* map, const void* base, long long cols, long l
   return tc::make_map(map, base, cols, rows, batches, ld, batch_stride, box_rows);
 }
 
-int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
+// One launch over rows [row0, m_end) of every member; pair = CTA-pair (2-CTA) tiles.
+static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_end, cudaStream_t s) {
   using namespace tc;
-  ARMT_REQUIRE(a.K % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs K %% 8 == 0 (K=%d)", a.K);
-  ARMT_REQUIRE(a.lda % 8 == 0 && a.ldb % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs lda/ldb %% 8 == 0");
-  if (a.epilogue == ARMT_EPI_SWIGLU)
-    ARMT_REQUIRE((a.swiglu_block == 32 || a.swiglu_block == 128) && a.N % (2 * a.swiglu_block) == 0,
-                 ARMT_ERR_UNSUPPORTED, "SwiGLU block must be 32 or 128 and divide N/2");
-  const int bn = pick_bn(a);
   int max_a = 0, max_b = 0;
   for (int g = 0; g < a.G; ++g) {
     max_a = a.a_slot[g] > max_a ? a.a_slot[g] : max_a;
@@ -553,13 +662,14 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   CUtensorMap ma, mb;
   int rc = make_map(&ma, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM);
   if (rc) return rc;
-  rc = make_map(&mb, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, bn);
+  rc = make_map(&mb, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, pair ? bn / 2 : bn);
   if (rc) return rc;
 
   Params p;
   memset(&p, 0, sizeof(p));
-  p.G = a.G; p.M = a.M; p.N = a.N; p.K = a.K;
-  p.tiles_m = (a.M + BM - 1) / BM;
+  const int tm = pair ? 2 * BM : BM;
+  p.G = a.G; p.M = m_end; p.N = a.N; p.K = a.K; p.row0 = row0;
+  p.tiles_m = (m_end - row0 + tm - 1) / tm;
   p.tiles_n = (a.N + bn - 1) / bn;
   p.num_tiles = a.G * p.tiles_m * p.tiles_n;
   p.k_blocks = (a.K + BK - 1) / BK;
@@ -574,19 +684,66 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   p.lse_tgt = a.lse_tgt; p.lse_rows = a.lse_rows;
   p.den = a.den; p.den_stride = a.den_stride; p.eps = a.eps;
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
+  p.rope_ld = a.M;  // tables are (head_dim/2, M): one column per position of the full member
   p.swiglu_block = a.swiglu_block;
   p.max_ctas = a.max_ctas;
+  {
+    const char* f = getenv("ARMT_GEMM_PF");
+    p.pf = f ? atoi(f) : 0;
+    const char* fa = getenv("ARMT_GEMM_PF_A");
+    p.pf_a = fa ? atoi(fa) : 0;
+  }
+  {
+    static const bool prof = getenv("ARMT_GEMM_PROF") != nullptr;
+    p.prof = prof ? 1 : 0;
+  }
   for (int g = 0; g < a.G; ++g) {
     p.a_slot[g] = (short)a.a_slot[g];
     p.b_index[g] = (short)a.b_index[g];
     p.c_slot[g] = (short)a.c_slot[g];
   }
   switch (bn) {
-    case 64: return dispatch_epi<64>(a, ma, mb, p, s);
-    case 128: return dispatch_epi<128>(a, ma, mb, p, s);
-    case 256: return dispatch_epi<256>(a, ma, mb, p, s);
+    case 64: return dispatch_epi<64, false>(a, ma, mb, p, s);
+    case 128: return dispatch_epi<128, false>(a, ma, mb, p, s);
+    case 256: return pair ? dispatch_epi<256, true>(a, ma, mb, p, s) : dispatch_epi<256, false>(a, ma, mb, p, s);
   }
   return ARMT_ERR_UNSUPPORTED;
 }
 
+int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
+  ARMT_REQUIRE(a.K % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs K %% 8 == 0 (K=%d)", a.K);
+  ARMT_REQUIRE(a.lda % 8 == 0 && a.ldb % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs lda/ldb %% 8 == 0");
+  if (a.epilogue == ARMT_EPI_SWIGLU)
+    ARMT_REQUIRE((a.swiglu_block == 32 || a.swiglu_block == 128) && a.N % (2 * a.swiglu_block) == 0,
+                 ARMT_ERR_UNSUPPORTED, "SwiGLU block must be 32 or 128 and divide N/2");
+  const int bn = tc::pick_bn(a);
+  // CTA-pair (cta_group::2, 256-row tiles) for mainloop-bound 256-wide GEMMs: rows
+  // [0, 256*floor(M/256)) as pair tiles, the remainder as single-CTA tiles (no padded
+  // MMA work). Epilogue-bound shapes (short-K residual/retrieve) stay single-CTA.
+  // ARMT_GEMM_PAIR=0 disables pairs (A/B runs).
+  const char* pe = getenv("ARMT_GEMM_PAIR");
+  const bool heavy_epi = a.epilogue == ARMT_EPI_RESIDUAL || a.epilogue == ARMT_EPI_RETRIEVE;
+  const int m_pair = (a.M / (2 * tc::BM)) * (2 * tc::BM);
+  // pairs only where M fills whole pair tiles (the LM head); ARMT_GEMM_PAIR=split also
+  // splits 1152-row members into 4 pair tiles + a single-CTA remainder launch (measured
+  // at base clocks: down -3%, qkv -1.5%, gate/up +7% -- not worth it by default)
+  const bool split = pe && strcmp(pe, "split") == 0;
+  const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split) &&
+                    a.K >= (heavy_epi ? 4096 : 1024) && !(pe && pe[0] == '0');
+  if (!pair) return gemm_rows(a, bn, false, 0, a.M, s);
+  int rc = gemm_rows(a, bn, true, 0, m_pair, s);
+  if (rc || m_pair == a.M) return rc;
+  return gemm_rows(a, bn, false, m_pair, a.M, s);
+}
+
 }  // namespace armt
+
+// Read (and optionally reset) the ARMT_GEMM_PROF wait-cycle counters (diagnostics).
+extern "C" int armt_gemm_prof(unsigned long long* out8, int reset) {
+  cudaMemcpyFromSymbol(out8, armt::tc::g_gemm_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(armt::tc::g_gemm_prof, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}

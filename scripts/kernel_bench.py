@@ -17,6 +17,8 @@ import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if "--prof" in sys.argv:
+    os.environ["ARMT_GEMM_PROF"] = "1"   # read once by the library
 sys.path.insert(0, ROOT)
 from paper_2506_05229_b200 import _lib  # noqa: E402
 from paper_2506_05229_b200._lib import BF16, F32  # noqa: E402
@@ -86,40 +88,58 @@ def gemm(G, Mr, N, K, epi=_lib.EPI_STORE, c_dtype=BF16, **kw):
     return (lambda: _lib.check(LIB.armt_gemm(a, s), "gemm")), 2.0 * G * Mr * N * K, keep
 
 
+def gemm_specs(G, rows=None):
+    R = rows or T
+    return {"gu": (G, R, 2 * F, d, _lib.EPI_SWIGLU, BF16), "down": (G, R, d, F, _lib.EPI_RESIDUAL, F32),
+            "qkv": (G, R, 3 * d, d, _lib.EPI_ROPE, BF16), "o": (G, R, d, d, _lib.EPI_RESIDUAL, F32),
+            "kvb": (G, M, 2128, d, _lib.EPI_STORE, F32), "num": (G, R, d, 384, _lib.EPI_RETRIEVE, F32),
+            "lm": (1, 1024, V, d, _lib.EPI_STORE, BF16)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--G", type=int, default=16)
     ap.add_argument("--ops", default="gu,down,qkv,o,kvb,num,attn,fold,foldtc,lm")
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--flags", default=None, help="A/B: comma list of ARMT_GEMM_FLAGS values, interleaved")
+    ap.add_argument("--flags", default=None, help="A/B: comma list of values of env var --env, interleaved")
+    ap.add_argument("--env", default="ARMT_GEMM_PAIR")
+    ap.add_argument("--rows", type=int, default=None, help="rows per member (default T)")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--prof", action="store_true", help="GEMM wait-cycle counters (ARMT_GEMM_PROF)")
     args = ap.parse_args()
     if args.flags:
         for rep in range(args.repeat):
             for fl in args.flags.split(","):
-                os.environ["ARMT_GEMM_FLAGS"] = fl
+                os.environ[args.env] = fl
                 for op in args.ops.split(","):
-                    spec = {"down": (G_ := args.G, T, d, F, _lib.EPI_RESIDUAL, F32),
-                            "o": (G_, T, d, d, _lib.EPI_RESIDUAL, F32),
-                            "num": (G_, T, d, 384, _lib.EPI_RETRIEVE, F32)}[op]
+                    spec = gemm_specs(args.G, args.rows)[op]
                     fn, flops, keep = gemm(*spec)
                     us = timeit(fn, args.iters)
-                    print(json.dumps({"op": op, "flags": fl, "rep": rep, "us": round(us, 1)}), flush=True)
+                    print(json.dumps({"op": op, args.env: fl, "rep": rep, "us": round(us, 1),
+                                      "tflops": round(flops / us / 1e6, 1)}), flush=True)
                     del keep
         return
     G = args.G
     pk = peaks()
     for op in args.ops.split(","):
         if op in ("gu", "down", "qkv", "o", "kvb", "num", "lm"):
-            spec = {"gu": (G, T, 2 * F, d, _lib.EPI_SWIGLU, BF16), "down": (G, T, d, F, _lib.EPI_RESIDUAL, F32),
-                    "qkv": (G, T, 3 * d, d, _lib.EPI_ROPE, BF16), "o": (G, T, d, d, _lib.EPI_RESIDUAL, F32),
-                    "kvb": (G, M, 2128, d, _lib.EPI_STORE, F32), "num": (G, T, d, 384, _lib.EPI_RETRIEVE, F32),
-                    "lm": (1, 1024, V, d, _lib.EPI_STORE, BF16)}[op]
+            spec = gemm_specs(G)[op]
             fn, flops, keep = gemm(*spec)
             us = timeit(fn, args.iters)
             tf = flops / us / 1e6
-            print(json.dumps({"op": op, "G": spec[0], "us": us, "tflops": tf,
-                              "frac_sustained": tf / pk["bf16_tflops_sustained"]}), flush=True)
+            rec = {"op": op, "G": spec[0], "us": us, "tflops": tf, "frac_sustained": tf / pk["bf16_tflops_sustained"]}
+            if args.prof:
+                import ctypes
+                buf = (ctypes.c_ulonglong * 8)()
+                LIB.armt_gemm_prof(buf, 1)
+                fn()
+                torch.cuda.synchronize()
+                LIB.armt_gemm_prof(buf, 1)
+                tot = max(buf[2], 1)
+                rec.update(mma_wait_full=buf[0] / tot, mma_wait_acc=buf[1] / tot, prod_wait_empty=buf[3] / tot,
+                           tiles=buf[4], epi_wait_full_per_tile=buf[5] / max(buf[4], 1) / 8,
+                           mma_cycles_per_cta=tot / min(148, buf[4]))
+            print(json.dumps(rec), flush=True)
         elif op == "attn":
             qkv = torch.randn(G, T, 3 * d, device="cuda").bfloat16()
             ctx = torch.empty(G, T, d, device="cuda", dtype=torch.bfloat16)

@@ -293,3 +293,68 @@ def test_logits_nll_matches_log_softmax(dtype, V):
                                    out.data_ptr(), rows, V, stream()), "nll")
     want = -torch.log_softmax(logits.double(), -1).gather(1, tgt[:, None])[:, 0]
     assert rel(out, want) < 1e-5
+
+
+@pytest.mark.parametrize("epi", ["store", "residual", "rope", "swiglu", "lse"])
+def test_tc_gemm_cta_pair_matches_single_cta(epi, monkeypatch):
+    """The CTA-pair (cta_group::2, 256-row) tiles plus the single-CTA remainder
+    launch must reproduce the single-CTA kernel at a C2 member height (1152
+    rows = 4 pair tiles + 128 remainder rows) for every epilogue."""
+    torch.manual_seed(7)
+    G, M = 3, 1152
+    K = 4096 if epi == "residual" else 1024
+    dh, H = 64, 4
+    N = {"store": 512, "residual": 512, "rope": 3 * H * dh, "swiglu": 1024, "lse": 1000}[epi]
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = (torch.randn(G, N, K, device=DEV) * 0.05).bfloat16()
+    monkeypatch.setenv("ARMT_GEMM_BN", "256")
+
+    def run(pair):
+        monkeypatch.setenv("ARMT_GEMM_PAIR", pair)
+        kw, outs = {}, []
+        if epi == "store":
+            C = torch.zeros(G, M, N, device=DEV)
+            args = gemm_args(G, M, N, K, A, B, C, BF16, F32)
+            outs = [C]
+        elif epi == "residual":
+            C = torch.randn(G, M, N, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
+            C2 = torch.zeros(G, M, N, device=DEV, dtype=torch.bfloat16)
+            ssq = torch.zeros(G, M, N // 64, device=DEV)
+            args = gemm_args(G, M, N, K, A, B, C, BF16, F32, epilogue=_lib.EPI_RESIDUAL, R=C.data_ptr(), ldr=N,
+                             r_stride=M * N, C2=C2.data_ptr(), ldc2=N, c2_stride=M * N, ssq_out=ssq.data_ptr(),
+                             ssq_stride=M * (N // 64), ssq_np=N // 64)
+            outs = [C, C2, ssq]
+        elif epi == "rope":
+            inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+            ang = np.arange(M)[:, None] * inv[None]
+            cos_t = torch.tensor(np.cos(ang).T.copy(), dtype=torch.float32, device=DEV)
+            sin_t = torch.tensor(np.sin(ang).T.copy(), dtype=torch.float32, device=DEV)
+            C = torch.zeros(G, M, N, device=DEV, dtype=torch.bfloat16)
+            args = gemm_args(G, M, N, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_ROPE, rope_cos=cos_t.data_ptr(),
+                             rope_sin=sin_t.data_ptr(), head_dim=dh, rope_cols=2 * H * dh)
+            outs = [C]
+            kw = {"keep": (cos_t, sin_t)}
+        elif epi == "swiglu":
+            C = torch.zeros(G, M, N // 2, device=DEV, dtype=torch.bfloat16)
+            args = gemm_args(G, M, N, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_SWIGLU, swiglu_block=128,
+                             ldc=N // 2, c_stride=M * N // 2)
+            outs = [C]
+        else:
+            tiles = -(-N // 256)
+            part = torch.zeros(M, tiles, 2, device=DEV)
+            tgt = torch.zeros(M, device=DEV)
+            ids = torch.randint(0, N, (M + 1,), device=DEV, generator=torch.Generator(DEV).manual_seed(2))
+            C = torch.zeros(1, device=DEV)
+            args = gemm_args(1, M, N, K, A, B, C, BF16, F32, epilogue=_lib.EPI_LSE, ldc=1, c_stride=0,
+                             lse_part=part.data_ptr(), lse_ld=tiles, targets=ids.data_ptr() + 8,
+                             lse_tgt=tgt.data_ptr(), lse_rows=M)
+            outs = [part, tgt]
+            kw = {"keep": ids}
+        _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+        torch.cuda.synchronize()
+        return [o.float().clone() for o in outs]
+
+    single, paired = run("0"), run("1")
+    for s_, p_ in zip(single, paired):
+        assert torch.isfinite(p_).all()
+        assert rel(p_, s_) < 1e-6, (epi, rel(p_, s_))
