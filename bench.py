@@ -252,7 +252,7 @@ def device_arm(args, rank, world):
     if args.segments is not None:
         n = args.segments * cfg.segment_size
     S = -(-n // cfg.segment_size)
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     t_setup = time.time()
     init = args.init or ("device" if args.config == "c5" else "reference")
@@ -262,7 +262,8 @@ def device_arm(args, rank, world):
 
     if world > 1 or args.force_sharded:
         from paper_2506_05229_b200.sharded import ShardedSession
-        sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule)
+        sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule,
+                              scoring=scoring_value)
     else:
         prep = prepare_weights(w, "bf16", dev)
         if init == "device":
@@ -288,7 +289,8 @@ def device_arm(args, rank, world):
             probe_events[-1][1].record()
 
     sess.warm_eager()
-    eng.probe = probe
+    sharded = world > 1 or args.force_sharded
+    eng.probe = None if sharded else probe   # (per-step graphs of the sharded path: no probe)
     sess.capture()
     eng.probe = None
     setup_s = time.time() - t_setup
@@ -327,10 +329,16 @@ def device_arm(args, rank, world):
     # Single GPU: a scoring Session fuses the next-token NLL into the LM-head epilogue
     # (no 33.6 GB logits round trip); the sharded path scores from the last rank's logits.
     launches_per_forward = sess.kernels_per_forward
-    if world == 1 and not scoring_value and not args.force_sharded:
+    if not scoring_value:
         del sess
         torch.cuda.empty_cache()
-        sess = Session(prep, n, schedule=args.schedule, scoring=True)
+        if world == 1 and not args.force_sharded:
+            sess = Session(prep, n, schedule=args.schedule, scoring=True)
+        else:
+            from paper_2506_05229_b200.sharded import ShardedSession
+            sess = ShardedSession(w, cfg, n, rank=rank, world=world, device=dev, schedule=args.schedule,
+                                  scoring=True)
+            sess._load_ids(torch.as_tensor(tokens).to(dev))
         sess.warm()
     host_ids = torch.as_tensor(tokens).pin_memory()
     host_nll = torch.empty(n - 1, dtype=torch.float32).pin_memory()
@@ -357,7 +365,7 @@ def device_arm(args, rank, world):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = n / (e2e_total / args.steps / 1e3)
-    mean_nll = float(host_nll.mean()) if rank == world - 1 else None
+    mean_nll = float(host_nll.mean())
 
     peaks, peak_kind = load_peaks()
     traffic = load_traffic() if (args.config == "c2" and full_g == 16) else None
@@ -407,7 +415,8 @@ def device_arm(args, rank, world):
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(n * 8),
                 "d2h_bytes_per_step": int((n - 1) * 4),
                 "api": "Session(scoring=True).nll: pinned ids in, per-token NLL out (LM-head fused NLL)"
-                       if world == 1 else "ShardedSession.nll: pinned ids in, per-token NLL out",
+                       if not sharded else "ShardedSession(scoring=True).nll: pinned ids in, per-token NLL out "
+                                          "(vocab-parallel fused NLL, all-gathered row partials)",
                 "mean_nll": mean_nll},
         "gpu_launches": int(launches_per_forward * args.steps),
         "clocks": clocks.summary(),
@@ -438,14 +447,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
-    if world > 1 or args.force_sharded:
+    if world > 1:
         import torch
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        # ARMT_DIST_BACKEND=gloo: plumbing runs with several ranks on one GPU (host-staged P2P)
+        torch.distributed.init_process_group(os.environ.get("ARMT_DIST_BACKEND", "nccl"))
     try:
         return device_arm(args, rank, world)
     finally:
-        if world > 1 or args.force_sharded:
+        if world > 1:
             import torch
             torch.distributed.destroy_process_group()
 

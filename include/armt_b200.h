@@ -172,6 +172,17 @@ int armt_logits_nll(const void* logits, int dtype, long long ld, const long long
 int armt_lse_finalize(const float* lse_part, long long lse_ld, int n_tiles, const float* tgt,
                       const long long* targets, float* nll, long long rows, void* stream);
 
+/* Reduce each row's n_tiles (max, sum) partials to one (max, sum) pair: out[r] (float2).
+ * Vocab-parallel LM head: per-rank reduction before the cross-rank all-gather, whose
+ * (rows, ranks) result armt_lse_finalize then turns into the NLL. */
+int armt_lse_reduce(const float* lse_part, long long lse_ld, int n_tiles, float* out, long long rows,
+                    void* stream);
+
+/* Diagnostics: with ARMT_GEMM_PROF set at load, the tcgen05 GEMM accumulates wait cycles
+ * ([0] MMA waiting for a full stage, [1] MMA waiting for a free accumulator, [2] MMA loop
+ * cycles, [3] producer waiting for an empty stage, [4] tiles, [5] epilogue waiting). */
+int armt_gemm_prof(unsigned long long* out8, int reset);
+
 /* Introspection. */
 const char* armt_last_error(void);
 const char* armt_version(void);

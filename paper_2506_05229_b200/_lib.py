@@ -25,7 +25,7 @@ EXPORTS = ("armt_gemm", "armt_embed", "armt_rmsnorm", "armt_dpfp_den", "armt_att
            "armt_rope", "armt_swiglu", "armt_mem_fold", "armt_fold_workspace_bytes", "armt_cast",
            "armt_logits_nll", "armt_last_error", "armt_version", "armt_num_sms",
            "armt_kernel_count", "armt_abi_sizeof", "armt_mem_fold_tc", "armt_fold_tc_workspace_bytes",
-           "armt_memop_rows", "armt_lse_finalize")
+           "armt_memop_rows", "armt_lse_finalize", "armt_lse_reduce", "armt_gemm_prof")
 
 _I = ctypes.c_int
 _LL = ctypes.c_longlong
@@ -92,6 +92,8 @@ def load(path: str = LIB_PATH):
         "armt_fold_tc_workspace_bytes": (_LL, [_I, _I, _I, _I]),
         "armt_memop_rows": (_LL, [_I, _I]),
         "armt_lse_finalize": (_I, [_P, _LL, _I, _P, _P, _P, _LL, _P]),
+        "armt_lse_reduce": (_I, [_P, _LL, _I, _P, _LL, _P]),
+        "armt_gemm_prof": (_I, [_P, _I]),
         "armt_cast": (_I, [_P, _I, _P, _I, _LL, _P]),
         "armt_logits_nll": (_I, [_P, _I, _LL, _P, _P, _LL, _I, _P]),
         "armt_last_error": (ctypes.c_char_p, []),

@@ -217,6 +217,27 @@ __global__ void lse_finalize_kernel(const float2* __restrict__ part, long long l
   if (lane == 0) nll[row] = targets[row] < 0 ? 0.f : 0.6931471805599453f * (M + log2f(S) - tgt[row]);
 }
 
+// (max, sum 2^(x - max)) of a row's n_tiles partials -> one partial per row
+// (vocab-parallel LM head: each rank reduces its block before the all-gather)
+__global__ void lse_reduce_kernel(const float2* __restrict__ part, long long ld, int n_tiles,
+                                  float2* __restrict__ out, long long rows) {
+  const long long row = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float2* pr = part + row * ld;
+  float M = -INFINITY;
+  for (int t = lane; t < n_tiles; t += 32) M = fmaxf(M, pr[t].x);
+  M = warp_max(M);
+  float S = 0.f;
+  if (M != -INFINITY)
+    for (int t = lane; t < n_tiles; t += 32) {
+      const float2 q = pr[t];
+      S += q.y * exp2f(q.x - M);
+    }
+  S = warp_sum(S);
+  if (lane == 0) out[row] = make_float2(M, S);
+}
+
 }  // namespace armt
 
 using namespace armt;
@@ -333,6 +354,15 @@ int armt_lse_finalize(const float* lse_part, long long lse_ld, int n_tiles, cons
   lse_finalize_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float2*>(lse_part), lse_ld, n_tiles, tgt, targets, nll, rows);
   ARMT_CHECK_LAUNCH("lse_finalize");
+  return ARMT_OK;
+}
+
+int armt_lse_reduce(const float* lse_part, long long lse_ld, int n_tiles, float* out, long long rows, void* stream) {
+  if (rows <= 0) return ARMT_OK;
+  ARMT_REQUIRE(lse_part && out && n_tiles >= 1, ARMT_ERR_INPUT, "lse_reduce: bad arguments");
+  lse_reduce_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float2*>(lse_part), lse_ld, n_tiles, reinterpret_cast<float2*>(out), rows);
+  ARMT_CHECK_LAUNCH("lse_reduce");
   return ARMT_OK;
 }
 

@@ -368,7 +368,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         if (live && row < p.lse_rows) {
           p.lse_part[(long long)row * p.lse_ld + nb] = make_float2(m, ssum);
-          if (tgt >= (long long)nb * BN && tgt < (long long)nb * BN + BN) p.lse_tgt[row] = tv;
+          if (tgt >= (long long)nb * BN && tgt < (long long)nb * BN + BN && tgt < p.N) p.lse_tgt[row] = tv;
         }
       } else if constexpr (EPI == E_SWIGLU) {
         const int out_n0 = nb * (BN / 2);

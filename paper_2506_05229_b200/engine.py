@@ -559,3 +559,35 @@ class Engine:
             self._tables(a, [slot], [0], [0])
         _lib.check(self.lib.armt_gemm(self._gemm(("lm", slot, out.data_ptr(), row0, max_ctas), fill), stream),
                    "unembed")
+
+    def unembed_block(self, a_ptr: int, a_ld: int, v0: int, v1: int, row0: int, stream: int,
+                      out: torch.Tensor | None = None, lse=None, key=None) -> None:
+        """LM head rows [row0, row0+seg) over the vocab block [v0, v1) (vocab-parallel
+        head of the layer-sharded path): A = seg x d bf16 rows at ``a_ptr`` (leading
+        dimension ``a_ld``). ``out`` = this rank's logits block (rows, v1-v0), or
+        ``lse`` = (part, tgt, targets_local, n_tokens) for the fused next-token NLL
+        partials (targets_local = ids - v0, so only this block's targets match)."""
+        p, cfg = self.p, self.cfg
+        d, V, seg = cfg.d_model, cfg.vocab_size, cfg.segment_size
+        nv = v1 - v0
+
+        def fill(a):
+            a.M, a.N, a.K, a.ab_dtype = seg, nv, d, p.ab
+            a.A, a.lda, a.a_stride = a_ptr, a_ld, seg * a_ld
+            a.B, a.ldb, a.b_stride = p.unemb.data_ptr() + v0 * d * p.unemb.element_size(), d, V * d
+            if lse is None:
+                odt = BF16 if out.dtype == torch.bfloat16 else F32
+                a.C, a.ldc, a.c_stride, a.c_dtype = out.data_ptr() + row0 * nv * out.element_size(), nv, seg * nv, odt
+                a.epilogue = EPI_STORE
+            else:
+                part, tgt, tloc, n_tokens = lse
+                tiles = part.shape[1]
+                rows = max(0, min(seg, n_tokens - 1 - row0))
+                a.C, a.ldc, a.c_stride, a.c_dtype = tgt.data_ptr(), 1, 0, F32
+                a.epilogue = _lib.EPI_LSE
+                a.lse_part, a.lse_ld = part.data_ptr() + row0 * tiles * 8, tiles
+                a.targets = tloc.data_ptr() + (row0 + 1) * 8
+                a.lse_tgt, a.lse_rows = tgt.data_ptr() + row0 * 4, rows
+            self._tables(a, [0], [0], [0])
+        k = ("blk", a_ptr, v0, v1, row0, None if out is None else out.data_ptr(), lse is None) if key is None else key
+        _lib.check(self.lib.armt_gemm(self._gemm(k, fill), stream), "unembed (vocab block)")

@@ -6,7 +6,17 @@ state (A, z never move). At global step i it runs the cells {(i-l, l) :
 l in [lo_r, hi_r)} as one grouped step. The only cross-rank edge is
 (s, lo_r - 1) -> (s, lo_r): after step i-1 rank r-1 sends the activation of
 segment s = i - lo_r (its last layer's output, T x d fp32) and rank r receives
-it before step i. Rank 0 embeds; the last rank runs the LM head.
+it before step i. Rank 0 embeds.
+
+The LM head is vocab-parallel: when segment s clears layer
+L-1 at step i, the last rank broadcasts its token rows (seg x d) at the start
+of step i+1 (after that step's receive, so every rank's point-to-point
+traffic of step i is posted before the collective: no cross-rank ordering
+deadlock), and every rank computes the logits of its contiguous vocab block
+(``vocab_blocks``). This spreads the 17% LM-head load over all ranks instead
+of stalling the pipeline on the last one, and shards the logits / NLL
+partials. Scoring sessions combine per-rank (max, sum-exp) row partials with
+one all-gather at the end.
 
 ``StagePlan`` is the per-rank integer bookkeeping (pure host logic, tested on
 CPU with world size 2 over gloo); ``run_stage`` drives any backend exposing
@@ -22,6 +32,14 @@ import numpy as np
 
 from .errors import InputError
 from .scheduler import Node, diagonal_members
+
+
+def vocab_blocks(vocab: int, world: int, align: int = 64) -> list[range]:
+    """Contiguous near-even vocab blocks, one per rank, starting on ``align``
+    multiples (each rank's NLL partial tiles are local to its block)."""
+    per = -(-vocab // world)
+    per = -(-per // align) * align
+    return [range(min(r * per, vocab), min((r + 1) * per, vocab)) for r in range(world)]
 
 
 def layer_blocks(n_layers: int, world: int) -> list[range]:
@@ -45,7 +63,8 @@ class StageStep:
     recv: tuple[int, int] | None   # (segment, slot) received from rank-1 before the step
     enter: tuple[int, int] | None  # (segment, slot) embedded before the step (rank 0)
     send: tuple[int, int] | None   # (segment, slot) sent to rank+1 after the step
-    exits: list[tuple[int, int]]   # (segment, slot) unembedded after the step (last rank)
+    exits: list[tuple[int, int]]   # (segment, slot) leaving layer L-1 at this step (last rank)
+    head: tuple[int, int | None] | None = None  # (segment, last-rank slot or None): every rank
 
 
 @dataclass
@@ -67,7 +86,10 @@ def stage_plan(n_segments: int, n_layers: int, rank: int, world: int) -> StagePl
     S, L = n_segments, n_layers
     blk = layer_blocks(L, world)[rank]
     lo, hi = blk.start, blk.stop
-    n_slots = max(1, min(S, hi - lo))
+    last = hi == L
+    # one spare slot: the exiting segment's rows stay intact until its deferred
+    # LM-head broadcast at the start of the next step (after that step's receive)
+    n_slots = max(1, min(S, hi - lo + 1))
     steps = []
     for i in range(S + L - 1):
         nodes = [n for n in diagonal_members(i, S, L) if lo <= n.layer < hi]
@@ -77,21 +99,37 @@ def stage_plan(n_segments: int, n_layers: int, rank: int, world: int) -> StagePl
         enter = (i, slot(i)) if lo == 0 and i < S else None
         s_out = i - (hi - 1)
         send = (s_out, slot(s_out)) if hi < L and 0 <= s_out < S else None
-        exits = [(s_out, slot(s_out))] if hi == L and 0 <= s_out < S else []
+        exits = [(s_out, slot(s_out))] if last and 0 <= s_out < S else []
+        s_exit = i - (L - 1)
+        head = (s_exit, slot(s_exit) if last else None) if 0 <= s_exit < S else None
         steps.append(StageStep(nodes, [slot(n.segment) for n in nodes], [n.layer for n in nodes],
-                               recv, enter, send, exits))
+                               recv, enter, send, exits, head))
     return StagePlan(rank, world, S, L, blk, n_slots, steps)
 
 
 def run_stage(plan: StagePlan, backend, comm) -> None:
-    """Drive one rank through every global step. ``comm`` has send(t, dst)
-    and recv(t, src) (torch.distributed P2P: NCCL on GPUs, gloo in tests)."""
-    r = plan.rank
+    """Drive one rank through every global step. ``comm`` has send(t, dst),
+    recv(t, src) and broadcast(t, src) (torch.distributed: NCCL on GPUs, gloo
+    in tests). ``backend`` exposes slot_tensor / after_recv / embed / step /
+    head_buffer / head."""
+    r, world = plan.rank, plan.world
+    pending = None
+
+    def head(h):
+        s, slot = h
+        buf = backend.head_buffer(slot)
+        if world > 1:
+            comm.broadcast(buf, world - 1)
+        backend.head(s, buf)
+
     for st in plan.steps:
         if st.recv is not None:
             s, slot = st.recv
             comm.recv(backend.slot_tensor(slot), r - 1)
             backend.after_recv(slot)
+        if pending is not None:
+            head(pending)
+            pending = None
         if st.enter is not None:
             s, slot = st.enter
             backend.embed(s, slot)
@@ -100,21 +138,55 @@ def run_stage(plan: StagePlan, backend, comm) -> None:
         if st.send is not None:
             s, slot = st.send
             comm.send(backend.slot_tensor(slot), r + 1)
-        for s, slot in st.exits:
-            backend.unembed(s, slot)
+        pending = st.head
+    if pending is not None:
+        head(pending)
 
 
 class TorchP2P:
-    """Point-to-point activation hand-off over torch.distributed."""
+    """Point-to-point activation hand-off and the LM-head broadcast over
+    torch.distributed. NCCL moves device tensors directly (NVLink); under gloo
+    (CPU tests, or several ranks sharing one GPU for plumbing checks) device
+    tensors are staged through host memory."""
 
     def __init__(self, dist):
         self.dist = dist
+        self.staged = dist.get_backend() == "gloo"
+
+    def _op(self, fn, t, peer, inplace):
+        if self.staged and t.is_cuda:
+            h = t.detach().to("cpu")
+            fn(h, peer)
+            if inplace:
+                t.copy_(h)
+        else:
+            fn(t, peer)
 
     def send(self, t, dst):
-        self.dist.send(t, dst)
+        self._op(self.dist.send, t, dst, False)
 
     def recv(self, t, src):
-        self.dist.recv(t, src)
+        self._op(self.dist.recv, t, src, True)
+
+    def broadcast(self, t, src):
+        self._op(lambda x, s: self.dist.broadcast(x, s), t, src, True)
+
+    def all_gather(self, out_list, t):
+        if self.staged and t.is_cuda:
+            hl = [torch_empty_like_cpu(x) for x in out_list]
+            self.dist.all_gather(hl, t.detach().to("cpu"))
+            for o, h in zip(out_list, hl):
+                o.copy_(h)
+        else:
+            self.dist.all_gather(out_list, t)
+
+    def all_reduce(self, t):
+        self._op(lambda x, _: self.dist.all_reduce(x), t, None, True)
+
+
+def torch_empty_like_cpu(x):
+    import torch
+    return torch.empty(x.shape, dtype=x.dtype)
 
 
 # ---------------------------------------------------------------------------
@@ -122,13 +194,42 @@ class TorchP2P:
 # ---------------------------------------------------------------------------
 
 class DeviceBackend:
-    def __init__(self, engine, runner_ids, logits, state, seg: int, stream_fn):
+    """CUDA ``Engine`` behind ``run_stage``. With ``graphs`` set, each embed /
+    step / head launch sequence is captured once (``mode='capture'``) and then
+    replayed as one CUDA graph (``mode='replay'``); the NCCL hand-offs between
+    them stay eager."""
+
+    def __init__(self, engine, runner_ids, logits, state, seg: int, stream_fn, vocab: range | None = None,
+                 head_in=None, lse=None):
         self.e = engine
         self.ids = runner_ids
         self.logits = logits
         self.state = state
         self.seg = seg
         self.stream = stream_fn
+        V = engine.cfg.vocab_size
+        self.vocab = vocab if vocab is not None else range(0, V)
+        self.head_in = head_in
+        self.lse = lse
+        self.mode = "eager"
+        self.graphs: dict = {}
+        self.step_no = 0
+
+    def _run(self, key, fn):
+        import torch
+        if self.mode == "eager":
+            fn()
+        elif self.mode == "capture":
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    fn()
+            torch.cuda.current_stream().wait_stream(side)
+            self.graphs[key] = g
+        else:
+            self.graphs[key].replay()
 
     def slot_tensor(self, slot):
         return self.e.xs[slot]
@@ -137,24 +238,51 @@ class DeviceBackend:
         from . import _lib
         if self.e.xs_bf is not None:
             x = self.e.xs[slot]
-            _lib.check(_lib.load().armt_cast(x.data_ptr(), _lib.F32, self.e.xs_bf[slot].data_ptr(), _lib.BF16,
-                                             x.numel(), self.stream()), "cast")
+            self._run(("cast", slot), lambda: _lib.check(_lib.load().armt_cast(
+                x.data_ptr(), _lib.F32, self.e.xs_bf[slot].data_ptr(), _lib.BF16, x.numel(), self.stream()), "cast"))
 
     def embed(self, s, slot):
-        self.e.embed(self.ids[s * self.seg:(s + 1) * self.seg], slot, self.stream())
+        self._run(("embed", s), lambda: self.e.embed(self.ids[s * self.seg:(s + 1) * self.seg], slot, self.stream()))
 
     def step(self, slots, layers):
-        self.e.step(slots, layers, self.state, self.stream())
+        self._run(("step", tuple(slots), tuple(layers)),
+                  lambda: self.e.step(slots, layers, self.state, self.stream()))
 
+    def head_buffer(self, slot):
+        """Token rows of the exiting segment: the last rank's slot (bf16 copy), or
+        this rank's receive buffer for the broadcast."""
+        if slot is not None:
+            return self.e.xs_bf[slot][:self.seg]
+        return self.head_in
+
+    def head(self, s, buf):
+        v0, v1 = self.vocab.start, self.vocab.stop
+        if v1 <= v0:
+            return
+        ptr, ld = buf.data_ptr(), buf.shape[-1]
+        if self.lse is not None:
+            self._run(("head", s, ptr), lambda: self.e.unembed_block(ptr, ld, v0, v1, s * self.seg, self.stream(),
+                                                                   lse=self.lse))
+        else:
+            self._run(("head", s, ptr), lambda: self.e.unembed_block(ptr, ld, v0, v1, s * self.seg, self.stream(),
+                                                                   out=self.logits))
+
+    # single-rank compatibility (tests/test_gpu_sharded.py drives stages by hand)
     def unembed(self, s, slot):
-        self.e.unembed(slot, self.logits, s * self.seg, self.stream())
+        self.head(s, self.head_buffer(slot))
 
 
 class ShardedSession:
-    """Session (executors.Session API) for one rank of a layer-sharded run."""
+    """Session (executors.Session API) for one rank of a layer-sharded run.
+
+    ``forward`` returns this rank's vocab block of the logits (vocab-parallel
+    LM head; ``vocab`` is the block); a ``scoring`` session keeps only the
+    fused next-token NLL partials and ``nll`` returns the full per-token NLL
+    on every rank (one all-gather of per-row (max, sum) pairs + one
+    all-reduce of the target logits)."""
 
     def __init__(self, weights, cfg, n_tokens: int, rank: int, world: int, device=None,
-                 schedule: str = "diagonal"):
+                 schedule: str = "diagonal", scoring: bool = False, graphs: bool = True):
         import torch
         import torch.distributed as dist
         from .engine import Engine, MemoryState, prepare_weights
@@ -162,20 +290,35 @@ class ShardedSession:
             raise InputError("layer sharding pipelines the diagonal schedule only")
         self.cfg, self.n, self.rank, self.world = cfg, int(n_tokens), rank, world
         S = -(-self.n // cfg.segment_size)
+        seg = cfg.segment_size
         self.plan = stage_plan(S, cfg.n_layers, rank, world)
         blk = self.plan.layers
         self.p = prepare_weights(weights, "bf16", device, layers=blk)
         dev = self.p.device
         self.engine = Engine(self.p, self.plan.max_members, self.plan.n_slots)
         self.state = MemoryState.fresh(cfg, dev, n_layers=len(blk))
-        self.ids = torch.zeros(S * cfg.segment_size, dtype=torch.int64, device=dev)
-        last = rank == world - 1
-        self.logits = (torch.empty(S * cfg.segment_size, cfg.vocab_size, dtype=torch.bfloat16, device=dev)
-                       if last else None)
-        self.nll_rows = torch.empty(max(self.n - 1, 1), device=dev) if last else None
-        self.backend = DeviceBackend(self.engine, self.ids, self.logits, self.state, cfg.segment_size,
-                                     lambda: torch.cuda.current_stream().cuda_stream)
-        self.comm = TorchP2P(dist)
+        self.ids = torch.zeros(S * seg, dtype=torch.int64, device=dev)
+        self.vocab = vocab_blocks(cfg.vocab_size, world)[rank]
+        nv = len(self.vocab)
+        self.scoring = scoring
+        self.logits = None
+        lse = None
+        if scoring:
+            tiles = max(1, -(-nv // 256))
+            self.lse_part = torch.empty(S * seg, tiles, 2, device=dev)
+            self.lse_tgt = torch.zeros(S * seg, device=dev)
+            self.ids_local = torch.zeros(S * seg, dtype=torch.int64, device=dev)
+            lse = (self.lse_part, self.lse_tgt, self.ids_local, self.n)
+            self.row_ms = torch.empty(S * seg, 2, device=dev)
+        else:
+            self.logits = torch.empty(S * seg, nv, dtype=torch.bfloat16, device=dev)
+        self.head_in = torch.empty(seg, cfg.d_model, dtype=torch.bfloat16, device=dev)
+        self.nll_rows = torch.empty(max(self.n - 1, 1), device=dev)
+        self.backend = DeviceBackend(self.engine, self.ids, self.logits, self.state, seg,
+                                     lambda: torch.cuda.current_stream().cuda_stream, vocab=self.vocab,
+                                     head_in=self.head_in, lse=lse)
+        self.comm = TorchP2P(dist) if world > 1 else None
+        self.use_graphs = graphs
         self.kernels_per_forward = None
 
         class _R:  # bench compatibility: sess.runner.engine
@@ -186,37 +329,75 @@ class ShardedSession:
     def _load_ids(self, tokens):
         import torch
         self.ids[:self.n].copy_(torch.as_tensor(tokens).reshape(-1).to(self.ids.device), non_blocking=True)
+        if self.n < self.ids.numel():
+            self.ids[self.n:].zero_()
+        if self.scoring:
+            torch.sub(self.ids, self.vocab.start, out=self.ids_local)
 
     def _forward(self):
         self.state.A.zero_()
         self.state.z.zero_()
         self.state.sync_shadow(self.p)
+        if self.scoring:
+            self.lse_tgt.zero_()
         run_stage(self.plan, self.backend, self.comm)
 
     def warm_eager(self):
         import torch
         from . import _lib
+        self.backend.mode = "eager"
         before = _lib.kernel_count()
         self._forward()
         torch.cuda.synchronize()
         self.kernels_per_forward = _lib.kernel_count() - before
 
     def capture(self):
-        """P2P hand-offs stay eager (NCCL send/recv per step); nothing to capture."""
+        """Capture every embed / step / head launch sequence as its own CUDA graph
+        (the capture pass executes nothing; NCCL hand-offs stay eager)."""
+        import torch
+        if not self.use_graphs:
+            return
+        self.backend.mode = "capture"
+        self._forward()
+        torch.cuda.synchronize()
+        self.backend.mode = "replay"
+
+    def warm(self):
+        self.warm_eager()
+        self.capture()
 
     def forward(self, tokens=None):
         if tokens is not None:
             self._load_ids(tokens)
         self._forward()
-        return None if self.logits is None else self.logits[:self.n]
+        return self.logits[:self.n] if self.logits is not None else None
 
     def nll(self, tokens=None):
+        """Per-token next-token NLL (n-1 values, device) on every rank."""
         import torch
         from . import _lib
-        logits = self.forward(tokens)
-        if logits is None:
-            return None
-        _lib.check(_lib.load().armt_logits_nll(logits.data_ptr(), _lib.BF16, self.cfg.vocab_size,
-                                               self.ids[1:self.n].data_ptr(), self.nll_rows.data_ptr(), self.n - 1,
-                                               self.cfg.vocab_size, torch.cuda.current_stream().cuda_stream), "nll")
-        return self.nll_rows[:self.n - 1]
+        if not self.scoring:
+            raise InputError("the sharded path scores through a scoring=True session (vocab-parallel NLL)")
+        self.forward(tokens)
+        lib = _lib.load()
+        st = torch.cuda.current_stream().cuda_stream
+        rows = self.n - 1
+        tiles = self.lse_part.shape[1]
+        if len(self.vocab):
+            _lib.check(lib.armt_lse_reduce(self.lse_part.data_ptr(), tiles, tiles, self.row_ms.data_ptr(), rows,
+                                           st), "lse_reduce")
+        else:  # empty vocab block (more ranks than 256-column tiles): neutral partials
+            self.row_ms[:, 0].fill_(float("-inf"))
+            self.row_ms[:, 1].zero_()
+        if self.world > 1:
+            parts = [torch.empty_like(self.row_ms) for _ in range(self.world)]
+            self.comm.all_gather(parts, self.row_ms)
+            ms = torch.stack(parts, 1).contiguous()           # (rows, ranks, 2)
+            tgt = self.lse_tgt.clone()
+            self.comm.all_reduce(tgt)                         # exactly one rank holds each target logit
+        else:
+            ms, tgt = self.row_ms[:, None, :].contiguous(), self.lse_tgt
+        _lib.check(lib.armt_lse_finalize(ms.data_ptr(), self.world, self.world, tgt.data_ptr(),
+                                         self.ids.data_ptr() + 8, self.nll_rows.data_ptr(), rows, st),
+                   "lse_finalize")
+        return self.nll_rows[:rows]

@@ -70,3 +70,133 @@ def test_local_pipeline_equals_unsharded(conf, eps, world):
     want, _ = run_diagonal(prepare_weights(w, "bf16"), cfg, tokens, state=st)
     assert np.array_equal(got, want)
     assert np.array_equal(A, st.A.cpu().numpy())
+
+
+def test_sharded_session_single_rank_matches_session():
+    """ShardedSession (per-step CUDA graphs, vocab-parallel head code path) at
+    world size 1 reproduces the single-GPU Session bitwise: logits and the
+    fused-NLL scoring output."""
+    from paper_2506_05229_b200.executors import Session
+    from paper_2506_05229_b200.sharded import ShardedSession
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    w = conditioned_weights(cfg)
+    n = 5 * cfg.segment_size - 3
+    tokens = torch.as_tensor(cli_tokens(cfg, n, seed=5)).cuda()
+    ref = Session(prepare_weights(w, "bf16"), n)
+    want = ref.forward(tokens).clone()
+    sh = ShardedSession(w, cfg, n, rank=0, world=1)
+    sh._load_ids(tokens)
+    sh.warm()
+    got = sh.forward()
+    assert torch.equal(got, want)
+    ref_s = Session(prepare_weights(w, "bf16"), n, scoring=True)
+    want_nll = ref_s.nll(tokens).clone()
+    sh_s = ShardedSession(w, cfg, n, rank=0, world=1, scoring=True)
+    sh_s._load_ids(tokens)
+    sh_s.warm()
+    got_nll = sh_s.nll()
+    assert torch.allclose(got_nll, want_nll, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_vocab_parallel_nll_combine_matches_full_vocab(P):
+    """Per-rank vocab blocks -> fused LSE partials -> per-row (max, sum) ->
+    cross-rank finalize equals the NLL of the full-vocab logits (the math of
+    ShardedSession.nll with the all-gather done in one process)."""
+    from paper_2506_05229_b200 import _lib
+    from paper_2506_05229_b200.sharded import vocab_blocks
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    w = conditioned_weights(cfg)
+    p = prepare_weights(w, "bf16")
+    eng = Engine(p, 1, 1)
+    seg, d, V = cfg.segment_size, cfg.d_model, cfg.vocab_size
+    torch.manual_seed(0)
+    x = torch.randn(seg, d, device="cuda").bfloat16()
+    n = seg + 1
+    ids = torch.randint(0, V, (n + seg,), device="cuda")
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    full = torch.empty(seg, V, dtype=torch.float32, device="cuda")
+    eng.unembed_block(x.data_ptr(), d, 0, V, 0, st, out=full)
+    want = torch.empty(seg, device="cuda")
+    _lib.check(lib.armt_logits_nll(full.data_ptr(), _lib.F32, V, ids[1:].data_ptr(), want.data_ptr(), seg, V, st), "nll")
+    ms = torch.empty(seg, P, 2, device="cuda")
+    tgt_sum = torch.zeros(seg, device="cuda")
+    for r, blk in enumerate(vocab_blocks(V, P)):
+        if not len(blk):
+            ms[:, r, 0] = float("-inf"); ms[:, r, 1] = 0
+            continue
+        tiles = -(-len(blk) // 256)
+        part = torch.empty(seg, tiles, 2, device="cuda")
+        tgt = torch.zeros(seg, device="cuda")
+        loc = ids - blk.start
+        eng.unembed_block(x.data_ptr(), d, blk.start, blk.stop, 0, st, lse=(part, tgt, loc, n))
+        row = torch.empty(seg, 2, device="cuda")
+        _lib.check(lib.armt_lse_reduce(part.data_ptr(), tiles, tiles, row.data_ptr(), seg, st), "reduce")
+        ms[:, r] = row
+        tgt_sum += tgt
+    got = torch.empty(seg, device="cuda")
+    _lib.check(lib.armt_lse_finalize(ms.data_ptr(), P, P, tgt_sum.data_ptr(), ids[1:].data_ptr(), got.data_ptr(),
+                                     seg, st), "finalize")
+    assert torch.allclose(got, want, rtol=1e-4, atol=1e-4), (got - want).abs().max()
+
+
+def _two_rank_worker(rank, world, port, out_q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    from conftest import MID as _MID
+    from fixtures import cli_tokens as _tok, conditioned_weights as _cw
+    from paper_2506_05229_b200.config import ModelConfig as _MC
+    from paper_2506_05229_b200.sharded import ShardedSession
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = _MC(**_MID, eps_assoc=10.0)
+    w = _cw(cfg)
+    n = 5 * cfg.segment_size - 3
+    tokens = torch.as_tensor(_tok(cfg, n, seed=5)).cuda()
+    sh = ShardedSession(w, cfg, n, rank=rank, world=world)
+    sh._load_ids(tokens)
+    sh.warm()
+    logits = sh.forward().float().cpu()
+    sc = ShardedSession(w, cfg, n, rank=rank, world=world, scoring=True)
+    sc._load_ids(tokens)
+    sc.warm()
+    nll = sc.nll().cpu()
+    out_q.put((rank, sh.vocab, logits, nll))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_pipeline_on_one_gpu_matches_single_session():
+    """World-size-2 layer-sharded run (two processes sharing this GPU, gloo
+    with host-staged hand-offs): the vocab-parallel logit blocks reassemble the
+    single-GPU logits bitwise and the all-gathered NLL matches."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2506_05229_b200.executors import Session
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, vocab, logits, nll = q.get(timeout=600)
+        res[r] = (vocab, logits, nll)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    w = conditioned_weights(cfg)
+    n = 5 * cfg.segment_size - 3
+    tokens = torch.as_tensor(cli_tokens(cfg, n, seed=5)).cuda()
+    want = Session(prepare_weights(w, "bf16"), n).forward(tokens).float().cpu()
+    got = torch.cat([res[0][1], res[1][1]], dim=1)
+    assert res[0][0].stop == res[1][0].start and got.shape == want.shape
+    assert torch.equal(got, want)
+    want_nll = Session(prepare_weights(w, "bf16"), n, scoring=True).nll(tokens).cpu()
+    for r in range(2):
+        assert torch.allclose(res[r][2], want_nll, rtol=1e-5, atol=1e-5)

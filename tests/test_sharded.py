@@ -18,7 +18,17 @@ import torch.multiprocessing as mp
 from conftest import C1
 from paper_2506_05229_b200.config import ModelConfig
 from paper_2506_05229_b200.scheduler import diagonal_members
-from paper_2506_05229_b200.sharded import TorchP2P, layer_blocks, run_stage, stage_plan
+from paper_2506_05229_b200.sharded import TorchP2P, layer_blocks, run_stage, stage_plan, vocab_blocks
+
+
+@pytest.mark.parametrize("V,P", [(256, 2), (128256, 8), (1000, 3), (300, 4), (50, 1)])
+def test_vocab_blocks_partition_and_align(V, P):
+    blocks = vocab_blocks(V, P)
+    assert len(blocks) == P and blocks[0].start == 0 and blocks[-1].stop == V
+    for a, b in zip(blocks, blocks[1:]):
+        assert a.stop == b.start
+    for b in blocks:
+        assert len(b) == 0 or b.start % 64 == 0
 
 
 @pytest.mark.parametrize("S,L,P", [(8, 16, 2), (128, 16, 8), (3, 5, 4), (1, 4, 4), (10, 7, 3), (5, 2, 1)])
@@ -34,6 +44,9 @@ def test_stage_plans_cover_the_wavefront(S, L, P):
                 assert plans[r - 1].steps[i - 1].send == (st.recv[0], plans[r - 1].steps[i - 1].send[1])
             if st.exits:
                 assert r == P - 1
+            # every rank joins the vocab-parallel head of the segment leaving layer L-1
+            s_exit = i - (L - 1)
+            assert st.head == ((s_exit, s_exit % p.n_slots if r == P - 1 else None) if 0 <= s_exit < S else None)
             if st.enter:
                 assert r == 0
             # no two in-flight segments share a slot on this rank
@@ -47,9 +60,11 @@ def test_stage_plans_cover_the_wavefront(S, L, P):
 class OracleBackend:
     """Test-only backend: oracle cells on CPU tensors (gloo moves them)."""
 
-    def __init__(self, orc, layers, n_slots, tokens):
+    def __init__(self, orc, layers, n_slots, tokens, vocab):
         import armt_oracle as O
         self.orc = orc
+        self.vocab = vocab
+        self.head_in = torch.zeros(orc.cfg.segment_size, orc.cfg.d_model, dtype=torch.float64)
         self.state = O.OracleState.fresh(orc.cfg, np.float64)
         self.slots = [torch.zeros(orc.T, orc.cfg.d_model, dtype=torch.float64) for _ in range(n_slots)]
         self.segs, self.n = O.segment_input(tokens, orc.cfg)
@@ -69,8 +84,11 @@ class OracleBackend:
             y = self.orc.cell(self.state, l, self.slots[slot].numpy().copy())
             self.slots[slot].copy_(torch.from_numpy(y))
 
-    def unembed(self, s, slot):
-        self.rows[s] = self.orc.unembed(self.slots[slot].numpy())
+    def head_buffer(self, slot):
+        return self.slots[slot][:self.orc.cfg.segment_size] if slot is not None else self.head_in
+
+    def head(self, s, buf):
+        self.rows[s] = buf.numpy() @ self.orc.unembedding[:, self.vocab.start:self.vocab.stop]
 
 
 def _worker(rank, world, port, tokens, out_q):
@@ -84,7 +102,7 @@ def _worker(rank, world, port, tokens, out_q):
     orc = O.Oracle(conditioned_weights(cfg), cfg, np.float64)
     S = len(tokens) // cfg.segment_size
     plan = stage_plan(S, cfg.n_layers, rank, world)
-    be = OracleBackend(orc, plan.layers, plan.n_slots, tokens)
+    be = OracleBackend(orc, plan.layers, plan.n_slots, tokens, vocab_blocks(cfg.vocab_size, world)[rank])
     run_stage(plan, be, TorchP2P(dist))
     own = [l for l in plan.layers]
     out_q.put((rank, be.rows, be.state.A[own].copy()))
@@ -121,8 +139,9 @@ def test_two_rank_gloo_pipeline_equals_unsharded_oracle():
         p.join(timeout=60)
         assert p.exitcode == 0
     want, wstate, _ = O.Oracle(conditioned_weights(cfg), cfg, np.float64).run_diagonal(tokens)
-    rows = results[1][0]
-    got = np.concatenate([rows[s] for s in range(5)])
-    assert np.array_equal(got, want)
+    # vocab-parallel head: rank r holds the logits of its vocab block for every segment
+    got = np.concatenate([np.concatenate([results[r][0][s] for s in range(5)]) for r in range(2)], axis=1)
+    assert got.shape == want.shape
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
     assert np.array_equal(results[0][1], wstate.A[0:1])
     assert np.array_equal(results[1][1], wstate.A[1:2])
