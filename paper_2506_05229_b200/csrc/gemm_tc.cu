@@ -652,7 +652,8 @@ int make_tma_map_bf16(CUtensorMap* map, const void* base, long long cols, long l
 }
 
 // One launch over rows [row0, m_end) of every member; pair = CTA-pair (2-CTA) tiles.
-static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_end, cudaStream_t s) {
+static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_end, cudaStream_t s,
+                     int max_ctas = -1) {
   using namespace tc;
   int max_a = 0, max_b = 0;
   for (int g = 0; g < a.G; ++g) {
@@ -686,7 +687,7 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.rope_cos = a.rope_cos; p.rope_sin = a.rope_sin; p.head_dim = a.head_dim; p.rope_cols = a.rope_cols;
   p.rope_ld = a.M;  // tables are (head_dim/2, M): one column per position of the full member
   p.swiglu_block = a.swiglu_block;
-  p.max_ctas = a.max_ctas;
+  p.max_ctas = max_ctas >= 0 ? max_ctas : a.max_ctas;
   {
     const char* f = getenv("ARMT_GEMM_PF");
     p.pf = f ? atoi(f) : 0;
@@ -724,16 +725,42 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   const char* pe = getenv("ARMT_GEMM_PAIR");
   const bool heavy_epi = a.epilogue == ARMT_EPI_RESIDUAL || a.epilogue == ARMT_EPI_RETRIEVE;
   const int m_pair = (a.M / (2 * tc::BM)) * (2 * tc::BM);
-  // pairs only where M fills whole pair tiles (the LM head); ARMT_GEMM_PAIR=split also
-  // splits 1152-row members into 4 pair tiles + a single-CTA remainder launch (measured
-  // at base clocks: down -3%, qkv -1.5%, gate/up +7% -- not worth it by default)
+  // Pairs where M fills whole pair tiles. ARMT_GEMM_PAIR=split also splits 1152-row members
+  // into 4 pair tiles + a single-CTA remainder launch after it (base clocks: down -3%, qkv
+  // -1.5%, gate/up +7% slower); ARMT_GEMM_PAIR=conc runs that remainder CONCURRENTLY on a
+  // forked stream with ARMT_GEMM_REM_CTAS SMs (default 20) while the pair tiles use the rest.
+  // Default policy (in-situ step breakdown, same box): whole-pair shapes -> pairs (LM head
+  // -11%); the QKV+RoPE GEMM -> concurrent remainder (-6%); gate/up and down stay single-CTA
+  // (pairs measured +2..4% slower there).
   const bool split = pe && strcmp(pe, "split") == 0;
-  const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split) &&
+  const bool conc = (pe && strcmp(pe, "conc") == 0) || (!pe && a.epilogue == ARMT_EPI_ROPE);
+  const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) &&
                     a.K >= (heavy_epi ? 4096 : 1024) && !(pe && pe[0] == '0');
   if (!pair) return gemm_rows(a, bn, false, 0, a.M, s);
-  int rc = gemm_rows(a, bn, true, 0, m_pair, s);
-  if (rc || m_pair == a.M) return rc;
-  return gemm_rows(a, bn, false, m_pair, a.M, s);
+  if (m_pair == a.M) return gemm_rows(a, bn, true, 0, m_pair, s);
+  if (!conc) {
+    int rc = gemm_rows(a, bn, true, 0, m_pair, s);
+    return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
+  }
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  if (side == nullptr) {
+    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+  }
+  const char* rc_env = getenv("ARMT_GEMM_REM_CTAS");
+  const int rem = rc_env ? atoi(rc_env) : 20;
+  const int sms = num_sms();
+  ARMT_REQUIRE(cudaEventRecord(fork_ev, s) == cudaSuccess, ARMT_ERR_CUDA, "gemm fork record");
+  ARMT_REQUIRE(cudaStreamWaitEvent(side, fork_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "gemm fork wait");
+  int rc = gemm_rows(a, bn, false, m_pair, a.M, side, rem);
+  if (rc) return rc;
+  rc = gemm_rows(a, bn, true, 0, m_pair, s, ((sms - rem) / 2) * 2);
+  if (rc) return rc;
+  ARMT_REQUIRE(cudaEventRecord(join_ev, side) == cudaSuccess, ARMT_ERR_CUDA, "gemm join record");
+  ARMT_REQUIRE(cudaStreamWaitEvent(s, join_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "gemm join wait");
+  return ARMT_OK;
 }
 
 }  // namespace armt
