@@ -55,6 +55,7 @@ struct Params {
   int max_ctas;
   int pf, pf_a;  // L2 prefetch distance in k-blocks for B (and A) tiles; 0 = off
   int row0;    // first row of every member this launch covers (rows [row0, M))
+  int xpose;   // residual/retrieve epilogue through the smem transpose (coalesced 128 B rows)
   int prof;    // ARMT_GEMM_PROF=1: accumulate wait cycles of the producer / MMA issuer
   short a_slot[ARMT_MAX_MEMBERS];
   short b_index[ARMT_MAX_MEMBERS];
@@ -72,6 +73,9 @@ template <int BN, bool PAIR = false> struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  // residual/retrieve epilogues: one 32 x 32 f32 transpose tile per epilogue warp
+  static constexpr int XPOSE_BYTES = 8 * 32 * 32 * 4;
+  static constexpr int SMEM_XPOSE = SMEM_BYTES + XPOSE_BYTES;
 };
 
 using namespace tcx;
@@ -171,6 +175,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  float4* xpose = reinterpret_cast<float4*>(smem + STAGES * C::STAGE_BYTES + 256);  // residual epilogues
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -439,6 +444,89 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           guarded = fabsf(den) <= p.eps;
           rden = 1.f / den;
         }
+        if constexpr (EPI == E_RESIDUAL || EPI == E_RETRIEVE) {
+          if (p.xpose) {
+            // Each 32 x 32 chunk: TMEM -> registers (lane = row) -> swizzled smem tile ->
+            // registers with lane = (row group, 4-column group): the residual load and the
+            // f32 / bf16 stores then move whole 128 B / 64 B row segments per 8 lanes
+            // (4x fewer L1 wavefronts than row-per-lane 16 B accesses).
+            float4* tb = xpose + (warp - 4) * 256;
+            const int m4 = lane & 7, rq = lane >> 3;
+            const int wrow0 = p.row0 + mb * TM + (int)rank * BM + ew * 32;
+            const float* rbase = p.R + (long long)c_slot * p.r_stride;
+            float* cbase = reinterpret_cast<float*>(p.C) + (long long)c_slot * p.c_stride;
+            __nv_bfloat16* c2base = p.C2 == nullptr ? nullptr : p.C2 + (long long)c_slot * p.c2_stride;
+            float sq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sq[k] = 0.f;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+              float v[32];
+              __syncwarp();
+              tmem_ld32(tbase + c0, v);
+              const int n0 = nb * BN + c0;
+              if (n0 >= p.N) break;  // warp-uniform
+              if constexpr (EPI == E_RETRIEVE) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = guarded ? 0.f : v[j] * rden;
+              }
+#pragma unroll
+              for (int c4 = 0; c4 < 8; ++c4)
+                tb[lane * 8 + (c4 ^ (lane & 7))] = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+              __syncwarp();
+              const int col = n0 + 4 * m4;
+              const bool cok = col < p.N;
+              float4 res[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int grow = wrow0 + rq + 4 * k;
+                res[k] = (cok && grow < p.M) ? *reinterpret_cast<const float4*>(rbase + (long long)grow * p.ldr + col)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int r = rq + 4 * k, grow = wrow0 + r;
+                const float4 a = tb[r * 8 + (m4 ^ (r & 7))];
+                float4 o;
+                o.x = res[k].x + a.x; o.y = res[k].y + a.y; o.z = res[k].z + a.z; o.w = res[k].w + a.w;
+                if (cok && grow < p.M) {
+                  *reinterpret_cast<float4*>(cbase + (long long)grow * p.ldc + col) = o;
+                  if (c2base != nullptr) {
+                    __nv_bfloat16* q = c2base + (long long)grow * p.ldc2 + col;
+                    const uint2 hi = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+                    *reinterpret_cast<uint2*>(q) = hi;
+                    if (p.c2_split > 0) {
+                      *reinterpret_cast<uint2*>(q + 2 * p.c2_split) = hi;
+                      const uint2 lo = make_uint2(
+                          pack_bf16x2(o.x - __bfloat162float(__float2bfloat16_rn(o.x)),
+                                      o.y - __bfloat162float(__float2bfloat16_rn(o.y))),
+                          pack_bf16x2(o.z - __bfloat162float(__float2bfloat16_rn(o.z)),
+                                      o.w - __bfloat162float(__float2bfloat16_rn(o.w))));
+                      *reinterpret_cast<uint2*>(q + p.c2_split) = lo;
+                    }
+                  }
+                }
+                sq[k] = fmaf(o.w, o.w, fmaf(o.z, o.z, fmaf(o.y, o.y, fmaf(o.x, o.x, sq[k]))));
+              }
+              __syncwarp();  // the tile is rewritten by the next chunk
+              if (p.ssq_out != nullptr && ((n0 & 63) == 32 || n0 + 32 >= p.N)) {
+                // row sums over the 8 lanes of each row group (fixed butterfly order)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  float t = sq[k];
+                  t += __shfl_xor_sync(0xffffffffu, t, 1);
+                  t += __shfl_xor_sync(0xffffffffu, t, 2);
+                  t += __shfl_xor_sync(0xffffffffu, t, 4);
+                  const int grow = wrow0 + rq + 4 * k;
+                  if (m4 == 0 && grow < p.M)
+                    p.ssq_out[(long long)g * p.ssq_stride + (long long)grow * p.ssq_np + (n0 >> 6)] = t;
+                  sq[k] = 0.f;
+                }
+              }
+            }
+            goto epi_done;
+          }
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
@@ -488,6 +576,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           }
         }
       }
+    epi_done:
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -551,7 +640,8 @@ static int make_map(CUtensorMap* map, const void* base, long long cols, long lon
 template <int BN, int EPI, int DH, bool PAIR>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
   auto kern = gemm_kernel<BN, EPI, DH, PAIR>;
-  constexpr int smem = Cfg<BN, PAIR>::SMEM_BYTES;
+  constexpr int smem = (EPI == E_RESIDUAL || EPI == E_RETRIEVE) ? Cfg<BN, PAIR>::SMEM_XPOSE
+                                                                 : Cfg<BN, PAIR>::SMEM_BYTES;
   static_assert(smem <= 227 * 1024, "GEMM shared memory budget");
   static bool attr_done = false;
   if (!attr_done) {
@@ -688,6 +778,16 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.rope_ld = a.M;  // tables are (head_dim/2, M): one column per position of the full member
   p.swiglu_block = a.swiglu_block;
   p.max_ctas = max_ctas >= 0 ? max_ctas : a.max_ctas;
+  {
+    // coalesced residual epilogue needs 16 B-aligned f32 rows and 8 B-aligned bf16 rows
+    const char* xe = getenv("ARMT_GEMM_XPOSE");
+    const bool al = (a.N % 4 == 0) && (a.ldc % 4 == 0) && (a.ldr % 4 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(a.C) | reinterpret_cast<uintptr_t>(a.R)) % 16 == 0) &&
+                    (a.C2 == nullptr || (a.ldc2 % 4 == 0 && a.c2_split % 4 == 0 &&
+                                         reinterpret_cast<uintptr_t>(a.C2) % 8 == 0)) &&
+                    (a.c_stride % 4 == 0) && (a.r_stride % 4 == 0) && (a.C2 == nullptr || a.c2_stride % 4 == 0);
+    p.xpose = al && !(xe && xe[0] == '0') ? 1 : 0;
+  }
   {
     const char* f = getenv("ARMT_GEMM_PF");
     p.pf = f ? atoi(f) : 0;
