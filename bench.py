@@ -69,14 +69,15 @@ def run_flops(cfg, n_segments: int) -> float:
     return n_segments * cfg.n_layers * cell_flops(cfg) + 2 * n_segments * cfg.segment_size * cfg.d_model * cfg.vocab_size
 
 
-def load_traffic():
+def load_traffic(key: str = "gemm_gu"):
     """DRAM bytes per gate/up launch from the committed ncu --set full capture
-    (profiles/*_kernels.json, written by scripts/profile_summary.py)."""
+    (profiles/*_kernels.json, written by scripts/profile_summary.py); ``key`` names
+    the capture (gemm_gu = 16 members, gemm_gu_g8 = 8 members, the dual-stream width)."""
     import glob
     best = None
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json"))):
         try:
-            m = json.load(open(path)).get("gemm_gu")
+            m = json.load(open(path)).get(key)
         except (OSError, ValueError):
             continue
         if m and "dram_read_bytes" in m:
@@ -273,26 +274,33 @@ def device_arm(args, rank, world):
     sess._load_ids(torch.as_tensor(tokens).to(dev))
 
     # roofline probe: events around every full-width gate/up GEMM, captured into the graph
+    # (dual-stream runner: each engine's full-width launches, on the stream they run on)
     probe_events = []
-    eng = sess.runner.engine
-    full_g = sess.plan.max_members
+    engines = getattr(sess.runner, "engines", [sess.runner.engine])
+    full_g = max(e.max_members for e in engines)
+    probe_g = engines[0].max_members
 
-    def probe(G, phase):
-        if G != full_g:
-            return
-        if phase == 0:
-            # external=True: event-record nodes that keep timing inside a CUDA graph
-            probe_events.append([torch.cuda.Event(enable_timing=True, external=True),
-                                 torch.cuda.Event(enable_timing=True, external=True)])
-            probe_events[-1][0].record()
-        else:
-            probe_events[-1][1].record()
+    def make_probe(e):
+        def probe(G, phase, stream=None):
+            if G != probe_g:
+                return
+            st = torch.cuda.ExternalStream(stream) if stream is not None else torch.cuda.current_stream()
+            if phase == 0:
+                # external=True: event-record nodes that keep timing inside a CUDA graph
+                probe_events.append([torch.cuda.Event(enable_timing=True, external=True),
+                                     torch.cuda.Event(enable_timing=True, external=True)])
+                probe_events[-1][0].record(st)
+            else:
+                probe_events[-1][1].record(st)
+        return probe
 
     sess.warm_eager()
     sharded = world > 1 or args.force_sharded
-    eng.probe = None if sharded else probe   # (per-step graphs of the sharded path: no probe)
+    for e in engines:
+        e.probe = None if sharded else make_probe(e)   # (per-step graphs of the sharded path: no probe)
     sess.capture()
-    eng.probe = None
+    for e in engines:
+        e.probe = None
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -368,12 +376,13 @@ def device_arm(args, rank, world):
     mean_nll = float(host_nll.mean())
 
     peaks, peak_kind = load_peaks()
-    traffic = load_traffic() if (args.config == "c2" and full_g == 16) else None
+    traffic = (load_traffic("gemm_gu" if probe_g == 16 else f"gemm_gu_g{probe_g}")
+               if (args.config == "c2" and full_g == 16) else None)
     d_ff_pad = sess.p.d_ff_pad
-    gu_bytes = 2.0 * (full_g * cfg.tokens_per_segment * cfg.d_model + full_g * 2 * d_ff_pad * cfg.d_model
-                      + full_g * cfg.tokens_per_segment * d_ff_pad)
+    gu_bytes = 2.0 * (probe_g * cfg.tokens_per_segment * cfg.d_model + probe_g * 2 * d_ff_pad * cfg.d_model
+                      + probe_g * cfg.tokens_per_segment * d_ff_pad)
     # dominant kernel: the grouped tcgen05 GEMM; probed launch = full-width gate/up (SwiGLU epilogue)
-    gu_flops = 2.0 * full_g * cfg.tokens_per_segment * (2 * d_ff_pad) * cfg.d_model
+    gu_flops = 2.0 * probe_g * cfg.tokens_per_segment * (2 * d_ff_pad) * cfg.d_model
     n_probe = len(probe_events)
     probe_avg_ms = statistics.mean(probe_ms) / max(n_probe, 1)
     achieved = gu_flops / (probe_avg_ms / 1e3) / 1e12 if n_probe else None
@@ -408,7 +417,7 @@ def device_arm(args, rank, world):
                      "traffic": (traffic or {}).get("bytes"),
                      "traffic_note": (f"DRAM bytes per launch (read+write) from {traffic['source']}; algorithmic "
                                       f"operand+output bytes {gu_bytes / 1e9:.3f} GB" if traffic else None),
-                     "kernel": f"tcgen05 grouped GEMM, gate/up (SwiGLU epilogue), G={full_g}, "
+                     "kernel": f"tcgen05 grouped GEMM, gate/up (SwiGLU epilogue), G={probe_g}, "
                                f"{gu_flops / 1e12:.3f} TFLOP/launch, {n_probe} launches/step",
                      "peak_kind": f"{peak_kind} bf16_tflops_sustained"},
         "cpu_baseline": cpu,

@@ -55,6 +55,7 @@ struct Params {
   int max_ctas;
   int pf, pf_a;  // L2 prefetch distance in k-blocks for B (and A) tiles; 0 = off
   int row0;    // first row of every member this launch covers (rows [row0, M))
+  int* tile_ctr;  // dynamic tile scheduling: {next tile, CTAs done} for this launch (nullptr = static)
   int xpose;   // residual/retrieve epilogue through the smem transpose (coalesced 128 B rows)
   int prof;    // ARMT_GEMM_PROF=1: accumulate wait cycles of the producer / MMA issuer
   short a_slot[ARMT_MAX_MEMBERS];
@@ -72,7 +73,7 @@ template <int BN, bool PAIR = false> struct Cfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 512 /*barriers, tile queue*/;
   // residual/retrieve epilogues: one 32 x 32 f32 transpose tile per epilogue warp
   static constexpr int XPOSE_BYTES = 8 * 32 * 32 * 4;
   static constexpr int SMEM_XPOSE = SMEM_BYTES + XPOSE_BYTES;
@@ -175,7 +176,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-  float4* xpose = reinterpret_cast<float4*>(smem + STAGES * C::STAGE_BYTES + 256);  // residual epilogues
+  float4* xpose = reinterpret_cast<float4*>(smem + STAGES * C::STAGE_BYTES + 512);  // residual epilogues
+  // dynamic tile queue (single-CTA mode): the producer claims tiles from a global counter
+  // and hands them to the MMA thread and the epilogue warpgroups through a smem ring
+  constexpr int QD = 8;
+  uint64_t* tq_full = bars + 2 * STAGES + 5;
+  uint64_t* tq_empty = tq_full + QD;
+  volatile int* tq_ids = reinterpret_cast<volatile int*>(tq_empty + QD);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,6 +197,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], PAIR ? 8 : 4); }
+    for (int i = 0; i < QD; ++i) { mbar_init(&tq_full[i], 1); mbar_init(&tq_empty[i], 5); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -210,13 +218,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles_mn = p.tiles_m * p.tiles_n;
+  const bool dyn = !PAIR && p.tile_ctr != nullptr;
+  // consumer side of the queue: entry k (MMA reads every k, epilogue group eg every k = eg mod 2)
+  auto tq_pop = [&](int k, bool epi_warp) -> int {
+    const int qs = k % QD;
+    mbar_wait(&tq_full[qs], (uint32_t)((k / QD) & 1));
+    const int t = tq_ids[qs];
+    if (!epi_warp || lane == 0) mbar_arrive(&tq_empty[qs]);
+    return t;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       int stage = 0; uint32_t phase = 0;
       unsigned long long w_empty = 0;
-      for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+      int qk = 0;
+      auto tq_push = [&](int t) {
+        const int qs = qk % QD;
+        mbar_wait(&tq_empty[qs], (uint32_t)(((qk / QD) & 1) ^ 1));
+        tq_ids[qs] = t;
+        mbar_arrive(&tq_full[qs]);
+        ++qk;
+      };
+      auto claim = [&]() -> int {
+        int t = atomicAdd(p.tile_ctr, 1);
+        if (t >= p.num_tiles) { tq_push(-1); tq_push(-1); return -1; }  // one sentinel per epilogue group
+        tq_push(t);
+        return t;
+      };
+      for (int tile = dyn ? claim() : (tile0 < p.num_tiles ? tile0 : -1); tile >= 0;
+           tile = dyn ? claim() : (tile + tstep < p.num_tiles ? tile + tstep : -1)) {
         const int g = tile / tiles_mn, r = tile - g * tiles_mn;
         const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
         const int a_slot = p.a_slot[g], b_idx = p.b_index[g];
@@ -249,6 +281,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       }
       if (p.prof) atomicAdd(&g_gemm_prof[3], w_empty);
+      if (dyn) {
+        // last CTA out resets the launch's counter pair (graph replays start from zero)
+        __threadfence();
+        if (atomicAdd(p.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
+          atomicExch(p.tile_ctr, 0);
+          atomicExch(p.tile_ctr + 1, 0);
+        }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -258,7 +298,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int acc = 0; uint32_t acc_phase = 0;
       unsigned long long w_full = 0, w_acc = 0, n_tiles = 0;
       const long long t_start = clock64();
-      for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+      int qk = 0;
+      for (int tile = dyn ? tq_pop(qk++, false) : (tile0 < p.num_tiles ? tile0 : -1); tile >= 0;
+           tile = dyn ? tq_pop(qk++, false) : (tile + tstep < p.num_tiles ? tile + tstep : -1)) {
         if (p.prof) {
           const long long t0 = clock64();
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -304,7 +346,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int eg = (warp - 4) >> 2;
     const int acc = eg;
     uint32_t acc_phase = 0;
-    for (int tile = tile0 + eg * tstep; tile < p.num_tiles; tile += 2 * tstep) {
+    int qk = eg;
+    auto first = [&]() { const int t = tile0 + eg * tstep; return t < p.num_tiles ? t : -1; };
+    for (int tile = dyn ? tq_pop(qk, true) : first(); tile >= 0;
+         tile = dyn ? tq_pop(qk += 2, true) : (tile + 2 * tstep < p.num_tiles ? tile + 2 * tstep : -1)) {
       const int g = tile / tiles_mn, r = tile - g * tiles_mn;
       const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
       const int row = p.row0 + mb * TM + (int)rank * BM + ew * 32 + lane;
@@ -778,6 +823,27 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.rope_ld = a.M;  // tables are (head_dim/2, M): one column per position of the full member
   p.swiglu_block = a.swiglu_block;
   p.max_ctas = max_ctas >= 0 ? max_ctas : a.max_ctas;
+  if (!pair) {
+    // dynamic tile scheduling: a fresh {next, done} counter pair per launch from a ring in
+    // device memory (each launch's last CTA re-zeroes its pair, so graph replays reuse it)
+    static int* ring = nullptr;
+    static unsigned long long next = 0;
+    constexpr unsigned long long RING = 1ull << 18;
+    static const bool dyn_on = !(getenv("ARMT_GEMM_DYN") && getenv("ARMT_GEMM_DYN")[0] == '0');
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    if (ring == nullptr) cudaStreamIsCapturing(s, &cap_st);   // (no allocation inside a graph capture)
+    if (dyn_on && (ring != nullptr || cap_st == cudaStreamCaptureStatusNone)) {
+      if (ring == nullptr) {
+        ARMT_REQUIRE(cudaMalloc(&ring, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring alloc");
+        ARMT_REQUIRE(cudaMemset(ring, 0, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring init");
+      }
+      p.tile_ctr = ring + 2 * (next++ % RING);
+    }
+  }
+  if (p.max_ctas == 0) {   // experiments: ARMT_GEMM_MAXCTAS caps every launch
+    static const char* mc = getenv("ARMT_GEMM_MAXCTAS");
+    if (mc) p.max_ctas = atoi(mc);
+  }
   {
     // coalesced residual epilogue needs 16 B-aligned f32 rows and 8 B-aligned bf16 rows
     const char* xe = getenv("ARMT_GEMM_XPOSE");
@@ -842,13 +908,27 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
     int rc = gemm_rows(a, bn, true, 0, m_pair, s);
     return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
   }
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-  if (side == nullptr) {
-    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+  // one forked stream per calling stream (callers on different streams stay independent)
+  struct Fork { cudaStream_t caller, side; cudaEvent_t fork_ev, join_ev; };
+  static Fork forks[8];
+  static int n_forks = 0;
+  static std::mutex fork_mu;
+  Fork* fk = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(fork_mu);
+    for (int i = 0; i < n_forks; ++i)
+      if (forks[i].caller == s) fk = &forks[i];
+    if (fk == nullptr) {
+      ARMT_REQUIRE(n_forks < 8, ARMT_ERR_UNSUPPORTED, "gemm: too many calling streams for the remainder fork");
+      fk = &forks[n_forks++];
+      fk->caller = s;
+      cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&fk->fork_ev, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&fk->join_ev, cudaEventDisableTiming);
+    }
   }
+  cudaStream_t side = fk->side;
+  cudaEvent_t fork_ev = fk->fork_ev, join_ev = fk->join_ev;
   const char* rc_env = getenv("ARMT_GEMM_REM_CTAS");
   const int rem = rc_env ? atoi(rc_env) : 20;
   const int sms = num_sms();

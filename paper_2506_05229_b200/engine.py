@@ -274,7 +274,7 @@ class Engine:
     """
 
     def __init__(self, prepared: PreparedWeights, max_members: int, n_slots: int,
-                 n_state_layers: int | None = None, fused_norm: bool = True):
+                 n_state_layers: int | None = None, fused_norm: bool = True, slots_from: "Engine | None" = None):
         p = prepared
         cfg = p.config
         self.p = p
@@ -287,8 +287,11 @@ class Engine:
         T, d, G = p.T, cfg.d_model, max_members
         wdt = p.wdtype
         self.bf16 = p.dtype_name == "bf16"
-        self.xs = torch.zeros(n_slots, T, d, device=dev)
-        self.xs_bf = torch.zeros(n_slots, T, d, dtype=torch.bfloat16, device=dev) if self.bf16 else None
+        if slots_from is not None:   # a second engine over the same activation slots (dual-stream runner)
+            self.xs, self.xs_bf = slots_from.xs, slots_from.xs_bf
+        else:
+            self.xs = torch.zeros(n_slots, T, d, device=dev)
+            self.xs_bf = torch.zeros(n_slots, T, d, dtype=torch.bfloat16, device=dev) if self.bf16 else None
         self.h = torch.empty(G, T, d, dtype=wdt, device=dev)
         self.qkv = torch.empty(G, T, 3 * d, dtype=wdt, device=dev)
         self.ctx = torch.empty(G, T, d, dtype=wdt, device=dev)
@@ -462,10 +465,10 @@ class Engine:
                 a.epilogue = EPI_STORE
             self._tables(a, a_idx, lrel, gid)
         if self.probe is not None:
-            self.probe(G, 0)
+            self.probe(G, 0, stream)
         _lib.check(lib.armt_gemm(self._gemm(("gu",) + key, fill_gu), stream), "gate/up")
         if self.probe is not None:
-            self.probe(G, 1)
+            self.probe(G, 1, stream)
         if not self.bf16:
             _lib.check(lib.armt_swiglu(G, self.gu_full.data_ptr(), 2 * F, T * 2 * F, self.gu.data_ptr(), F, T * F,
                                        F32, T, F, p.swiglu_block, stream), "swiglu")

@@ -189,6 +189,7 @@ def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = Non
 # latency-bound kernels, the next step's small launches)
 LM_FREE_SMS = int(__import__("os").environ.get("ARMT_LM_FREE_SMS", "16"))
 LM_OVERLAP = __import__("os").environ.get("ARMT_LM_OVERLAP", "0") == "1"
+DUAL = __import__("os").environ.get("ARMT_DUAL", "1") == "1"
 
 
 # =========================================================================
@@ -206,8 +207,24 @@ class Runner:
         self.plan = plan
         cfg = prepared.config
         self.cfg = cfg
-        self.engine = Engine(prepared, max(1, plan.max_members), plan.n_slots)
         dev = prepared.device
+        L = cfg.n_layers
+        # dual-stream wavefront (bf16 diagonal runs): layers [0, L/2) on the capture
+        # stream, [L/2, L) + the LM head on a second stream, so one half's latency-bound
+        # memory update overlaps the other half's tensor-core work (see _launch_dual)
+        self.dual = (DUAL and prepared.dtype_name == "bf16" and plan.kind == "diagonal" and L >= 2
+                     and plan.max_members >= 2)
+        if self.dual:
+            self.split = L // 2
+            g0 = max(1, max(sum(1 for l in st.layers if l < self.split) for st in plan.steps))
+            g1 = max(1, max(sum(1 for l in st.layers if l >= self.split) for st in plan.steps))
+            self.engine = Engine(prepared, g0, plan.n_slots)
+            self.engine2 = Engine(prepared, g1, plan.n_slots, slots_from=self.engine)
+            self.engines = [self.engine, self.engine2]
+            self.s1 = torch.cuda.Stream(device=dev)
+        else:
+            self.engine = Engine(prepared, max(1, plan.max_members), plan.n_slots)
+            self.engines = [self.engine]
         seg = cfg.segment_size
         self.ids = torch.zeros(plan.n_segments * seg, dtype=torch.int64, device=dev)
         self.scoring_tokens = scoring_tokens
@@ -232,7 +249,57 @@ class Runner:
         self.lm_ctas = max(1, int(_lib.load().armt_num_sms()) - LM_FREE_SMS)
         self.side = torch.cuda.Stream(device=dev) if self.lm_overlap else None
 
+    def _launch_dual(self, state: MemoryState, stream: int) -> None:
+        """Two-stream wavefront. Stream 0 runs each step's members with layer < L/2
+        (and embeds entering segments), stream 1 the members with layer >= L/2 and
+        the LM head of the exiting segment. Cross-stream edges: stream 1's step i
+        waits for stream 0's step i-1 (it consumes the segment that just left layer
+        L/2 - 1); an embed waits for the LM head of the slot's previous segment.
+        Memory state is per layer, so the halves never share it; every kernel is
+        member-lane independent, so results are bitwise those of the one-stream run."""
+        e0, e1 = self.engine, self.engine2
+        seg, split = self.cfg.segment_size, self.split
+        dev = self.p.device
+        cur = torch.cuda.ExternalStream(stream, device=dev)
+        s1 = self.s1
+        start = torch.cuda.Event()
+        start.record(cur)
+        s1.wait_event(start)
+        s1h = s1.cuda_stream
+        lm_done: dict[int, torch.cuda.Event] = {}
+        prev0 = None
+        for st in self.plan.steps:
+            sl0 = [(sl, l) for sl, l in zip(st.slots, st.layers) if l < split]
+            sl1 = [(sl, l) for sl, l in zip(st.slots, st.layers) if l >= split]
+            if st.enter is not None:
+                sg, slot = st.enter
+                if slot in lm_done:
+                    cur.wait_event(lm_done.pop(slot))
+                e0.embed(self.ids[sg * seg:(sg + 1) * seg], slot, stream)
+            if sl0:
+                e0.step([a for a, _ in sl0], [b for _, b in sl0], state, stream)
+            done0 = torch.cuda.Event()
+            done0.record(cur)
+            if prev0 is not None:
+                s1.wait_event(prev0)
+            prev0 = done0
+            if sl1:
+                e1.step([a for a, _ in sl1], [b for _, b in sl1], state, s1h)
+            for sg, slot in st.exits:
+                if self.scoring_tokens is not None:
+                    e1.unembed_lse(slot, self.ids, sg * seg, self.scoring_tokens, self.lse_part, self.lse_tgt, s1h)
+                else:
+                    e1.unembed(slot, self.logits, sg * seg, s1h)
+                ev = torch.cuda.Event()
+                ev.record(s1)
+                lm_done[slot] = ev
+        end = torch.cuda.Event()
+        end.record(s1)
+        cur.wait_event(end)
+
     def _launch_all(self, state: MemoryState, stream: int, events=None) -> None:
+        if self.dual and events is None:
+            return self._launch_dual(state, stream)
         """Issue every step. The LM head of an exiting segment runs on a side
         stream with ``lm_ctas`` CTAs, overlapping the memory update of its
         step and the following step(s) on the SMs it leaves free; the main
@@ -241,6 +308,8 @@ class Runner:
         seg = self.cfg.segment_size
         cur = torch.cuda.ExternalStream(stream, device=self.p.device)
         overlap = self.lm_overlap and events is None
+        if self.dual:   # timed (per-step events) replays run one stream over all members
+            eng = self._full_engine()
         pending: dict[int, torch.cuda.Event] = {}   # slot -> LM head done
         for i, st in enumerate(self.plan.steps):
             if events is not None:
@@ -277,6 +346,12 @@ class Runner:
         for ev in pending.values():
             cur.wait_event(ev)
 
+    def _full_engine(self):
+        """A one-stream engine over the same slots (timed per-step replays)."""
+        if getattr(self, "_full", None) is None:
+            self._full = Engine(self.p, max(1, self.plan.max_members), self.plan.n_slots, slots_from=self.engine)
+        return self._full
+
     def run(self, state: MemoryState, timed: bool = False) -> None:
         """Eager replay on the current stream (state mutated in place)."""
         stream = torch.cuda.current_stream().cuda_stream
@@ -301,7 +376,11 @@ class Runner:
                 if reset_state:
                     state.A.zero_()
                     state.z.zero_()
-                state.sync_shadow(self.p)
+                    if state.memop is None:
+                        state.sync_shadow(self.p)   # allocates the operand (setup)
+                    state.memop.zero_() if state.memop is not None else None  # split of a zero state is zero
+                else:
+                    state.sync_shadow(self.p)
                 self._launch_all(state, side.cuda_stream)
         torch.cuda.current_stream().wait_stream(side)
         self.graph = g

@@ -337,7 +337,10 @@ class ShardedSession:
     def _forward(self):
         self.state.A.zero_()
         self.state.z.zero_()
-        self.state.sync_shadow(self.p)
+        if self.state.memop is None:
+            self.state.sync_shadow(self.p)
+        else:
+            self.state.memop.zero_()   # bf16x3 split of the zero state
         if self.scoring:
             self.lse_tgt.zero_()
         run_stage(self.plan, self.backend, self.comm)
