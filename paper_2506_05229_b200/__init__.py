@@ -22,6 +22,10 @@ _LAZY = {
     "run_sequential": "executors", "run_diagonal": "executors", "segment_input": "executors",
     "relative_error": "executors", "ExecutionTrace": "executors", "TraceEvent": "executors",
     "Runner": "executors", "diagonal_plan": "executors", "sequential_plan": "executors",
+    "minibatch_plan": "executors", "run_minibatch": "executors", "Session": "executors",
+    "VerifyReport": "reports", "BenchReport": "reports", "verify": "reports", "bench": "reports",
+    "trace_document": "reports", "validate_report": "reports",
+    "ShardedSession": "sharded", "stage_plan": "sharded", "vocab_blocks": "sharded", "layer_blocks": "sharded",
     "SegmentActivation": "layers", "embed_segment": "layers", "unembed": "layers",
     "layer_forward": "layers", "grouped_layer_forward": "layers", "forward_stack": "layers",
     "retrieve_stack": "layers", "update_stack": "layers", "assoc_retrieve": "layers",

@@ -351,8 +351,14 @@ class Engine:
                                        cfg.num_mem_tokens, d, cfg.vocab_size, stream), "embed")
 
     # -- the three stacked cores ---------------------------------------------
-    def retrieve(self, slots, layers, state: MemoryState, stream: int) -> None:
-        """retrieve_stack (armt/memory.py:132-152), in place on xs[slots]."""
+    def retrieve(self, slots, layers, state: MemoryState, stream: int, state_layers=None) -> None:
+        """retrieve_stack (armt/memory.py:132-152), in place on xs[slots].
+
+        ``state_layers`` index the memory state (default: ``layers``); the
+        minibatch plan keeps one state block per copy (state layer b*L + l)
+        while the weights stay indexed by ``layers``."""
+        if state_layers is None:
+            state_layers = layers
         p, cfg, lib = self.p, self.cfg, self.lib
         T, d, G = p.T, cfg.d_model, len(layers)
         lrel = [l - self.layer_base for l in layers]
@@ -368,7 +374,8 @@ class Engine:
             self._tables(a, slots, lrel, gid)
         args = self._gemm(("q", tuple(slots), tuple(layers)), fill_q)
         _lib.check(lib.armt_gemm(args, stream), "retrieve q-proj")
-        mem = self._members(slots, layers)
+        srel = [l - self.layer_base for l in state_layers]
+        mem = self._members(slots, state_layers)
         _lib.check(lib.armt_dpfp_den(mem, self.qm.data_ptr(), T * cfg.d_mem, state.z.data_ptr(),
                                      self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
                                      self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
@@ -387,8 +394,8 @@ class Engine:
             if self.fused:
                 a.C2, a.ldc2, a.c2_stride = self.xs_bf.data_ptr(), d, T * d
                 a.ssq_out, a.ssq_stride, a.ssq_np = self.ssq_attn.data_ptr(), T * self.ssq_np, self.ssq_np
-            self._tables(a, gid, lrel, slots)
-        args = self._gemm(("num", tuple(slots), tuple(layers), bmat.data_ptr()), fill_n)
+            self._tables(a, gid, srel, slots)
+        args = self._gemm(("num", tuple(slots), tuple(state_layers), bmat.data_ptr()), fill_n)
         _lib.check(lib.armt_gemm(args, stream), "retrieve numerator")
 
     def forward(self, slots, layers, stream: int) -> None:
@@ -485,8 +492,11 @@ class Engine:
             self._tables(a, gid, lrel, slots)
         _lib.check(lib.armt_gemm(self._gemm(("down",) + key, fill_down), stream), "down-proj")
 
-    def update(self, slots, layers, state: MemoryState, stream: int) -> None:
-        """update_stack (armt/memory.py:155-180) from the memory rows of xs[slots]."""
+    def update(self, slots, layers, state: MemoryState, stream: int, state_layers=None) -> None:
+        """update_stack (armt/memory.py:155-180) from the memory rows of xs[slots]
+        (``state_layers``: see ``retrieve``)."""
+        if state_layers is None:
+            state_layers = layers
         p, cfg, lib = self.p, self.cfg, self.lib
         T, d, M = p.T, cfg.d_model, cfg.num_mem_tokens
         if M == 0:
@@ -504,7 +514,7 @@ class Engine:
             a.epilogue = EPI_STORE
             self._tables(a, slots, lrel, gid)
         _lib.check(lib.armt_gemm(self._gemm(("kvb", tuple(slots), tuple(layers)), fill_kvb), stream), "kvb")
-        mem = self._members(slots, layers)
+        mem = self._members(slots, state_layers)
         if self.bf16:
             _lib.check(lib.armt_mem_fold_tc(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off,
                                             p.b_off, state.A.data_ptr(), state.z.data_ptr(), state.memop.data_ptr(),
@@ -516,10 +526,10 @@ class Engine:
                                          cfg.d_mem, cfg.dpfp_nu, p.eps_assoc, self.fold_ws.data_ptr(), stream),
                        "mem_fold")
 
-    def step(self, slots, layers, state: MemoryState, stream: int) -> None:
-        self.retrieve(slots, layers, state, stream)
+    def step(self, slots, layers, state: MemoryState, stream: int, state_layers=None) -> None:
+        self.retrieve(slots, layers, state, stream, state_layers)
         self.forward(slots, layers, stream)
-        self.update(slots, layers, state, stream)
+        self.update(slots, layers, state, stream, state_layers)
 
     def unembed_lse(self, slot: int, ids: torch.Tensor, row0: int, n_tokens: int, part: torch.Tensor,
                     tgt: torch.Tensor, stream: int, max_ctas: int = 0) -> None:

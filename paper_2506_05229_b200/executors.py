@@ -111,6 +111,14 @@ class Step:
     layers: list[int]
     enter: tuple[int, int] | None  # (segment, slot) embedded before the step
     exits: list[tuple[int, int]]   # (segment, slot) unembedded after the step
+    # minibatch plans: one member per copy; the state is indexed per copy
+    state_layers: list[int] | None = None
+    more_enters: list[tuple[int, int]] = field(default_factory=list)
+    exit_rows: list[int] | None = None   # logits row of each exit (default segment * seg)
+
+    @property
+    def enters(self) -> list[tuple[int, int]]:
+        return ([self.enter] if self.enter is not None else []) + self.more_enters
 
 
 @dataclass
@@ -139,6 +147,27 @@ def sequential_plan(n_segments: int, n_layers: int) -> Plan:
             steps.append(Step([Node(s, l)], [k], [l], (s, k) if l == 0 else None,
                               [(s, k)] if l == n_layers - 1 else []))
     return Plan("sequential", n_segments, n_layers, n_slots, steps)
+
+
+def minibatch_plan(n_segments: int, n_layers: int, copies: int) -> Plan:
+    """The reference's minibatch axis (armt/cli.py:139-153): ``copies``
+    independent streams, each on the sequential schedule (row-major (s, l)).
+    On the device the copies advance in lockstep, so step (s, l) is ONE
+    grouped launch of ``copies`` members on layer l (shared weights); copy b
+    owns activation slot b and memory-state block b (state layer b*L + l).
+    Each copy's trace equals ``sequential_plan``'s."""
+    if copies < 1:
+        raise InputError(f"copies must be >= 1, got {copies}")
+    S, L, B = n_segments, n_layers, copies
+    steps = []
+    for s in range(S):
+        for l in range(L):
+            enters = [(s, b) for b in range(B)] if l == 0 else []
+            exits = [(s, b) for b in range(B)] if l == L - 1 else []
+            steps.append(Step([Node(s, l)] * B, list(range(B)), [l] * B, enters[0] if enters else None, exits,
+                              state_layers=[b * L + l for b in range(B)], more_enters=enters[1:],
+                              exit_rows=[b * S + s for b in range(B)] if exits else None))
+    return Plan("minibatch", S, L, B, steps)
 
 
 def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = None,
@@ -239,7 +268,8 @@ class Runner:
         else:
             if logits_dtype is None:
                 logits_dtype = torch.bfloat16 if prepared.dtype_name == "bf16" else torch.float32
-            self.logits = torch.empty(plan.n_segments * seg, cfg.vocab_size, dtype=logits_dtype, device=dev)
+            copies = plan.n_slots if plan.kind == "minibatch" else 1
+            self.logits = torch.empty(copies * plan.n_segments * seg, cfg.vocab_size, dtype=logits_dtype, device=dev)
         self.graph = None
         self.graph_state = None
         self.step_events = None
@@ -314,13 +344,12 @@ class Runner:
         for i, st in enumerate(self.plan.steps):
             if events is not None:
                 events[i][0].record()
-            if st.enter is not None:
-                s, slot = st.enter
+            for s, slot in st.enters:
                 if slot in pending:
                     cur.wait_event(pending.pop(slot))
                 eng.embed(self.ids[s * seg:(s + 1) * seg], slot, stream)
             if st.nodes:
-                eng.retrieve(st.slots, st.layers, state, stream)
+                eng.retrieve(st.slots, st.layers, state, stream, st.state_layers)
                 eng.forward(st.slots, st.layers, stream)
             lm_stream, ctas = stream, 0
             if st.exits and overlap:
@@ -328,19 +357,20 @@ class Runner:
                 ev.record(cur)
                 self.side.wait_event(ev)
                 lm_stream, ctas = self.side.cuda_stream, self.lm_ctas
-            for s, slot in st.exits:
+            for k, (s, slot) in enumerate(st.exits):
+                row = (st.exit_rows[k] if st.exit_rows is not None else s) * seg
                 if self.scoring_tokens is not None:
-                    eng.unembed_lse(slot, self.ids, s * seg, self.scoring_tokens, self.lse_part, self.lse_tgt,
+                    eng.unembed_lse(slot, self.ids, row, self.scoring_tokens, self.lse_part, self.lse_tgt,
                                     lm_stream, ctas)
                 else:
-                    eng.unembed(slot, self.logits, s * seg, lm_stream, ctas)
+                    eng.unembed(slot, self.logits, row, lm_stream, ctas)
             if st.exits and overlap:
                 done = torch.cuda.Event()
                 done.record(self.side)
                 for s, slot in st.exits:
                     pending[slot] = done
             if st.nodes:
-                eng.update(st.slots, st.layers, state, stream)
+                eng.update(st.slots, st.layers, state, stream, st.state_layers)
             if events is not None:
                 events[i][1].record()
         for ev in pending.values():
@@ -475,6 +505,42 @@ def run_diagonal(weights, config: ModelConfig, tokens, *, dtype: str = "bf16", t
         raise InputError(f"threads must be a positive int, got {threads!r}")
     return _run("diagonal", weights, config, tokens, dtype, state, shuffle_seed, device, graph,
                 return_numpy, timed)
+
+
+def run_minibatch(weights, config: ModelConfig, tokens, copies: int, *, dtype: str = "bf16",
+                  state: MemoryState | None = None, device=None, graph: bool = False, return_numpy: bool = True):
+    """The reference's minibatch comparison mode (armt/cli.py:139-153): ``copies``
+    independent streams of ``tokens``, each on the sequential schedule, run in
+    lockstep as one grouped launch per (segment, layer) with one member per copy.
+    Returns logits (copies, n, V) and the per-copy trace (sequential order).
+    ``state`` (optional) must hold copies * L layers (state layer b*L + l)."""
+    prepared = _prepared_for(weights, config, dtype, device)
+    segs, n = segment_input(tokens, config)
+    S, L = len(segs), config.n_layers
+    plan = minibatch_plan(S, L, copies)
+    if state is None:
+        state = MemoryState.fresh(config, prepared.device, n_layers=copies * L)
+    state.check_compatible(prepared, n_layers=copies * L)
+    runner = Runner(prepared, plan)
+    runner.ids.copy_(torch.as_tensor(np.concatenate(segs)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter_ns()
+    if graph:
+        runner.capture(state)
+        runner.replay()
+    else:
+        runner.run(state)
+    torch.cuda.synchronize()
+    total = time.perf_counter_ns() - t0
+    state.updates += S   # every (copy, layer) block folded once per segment
+    trace = ExecutionTrace(schedule_kind="minibatch")
+    for i, st in enumerate(plan.steps):
+        trace.events.append(TraceEvent(step=i, nodes=[st.nodes[0]], worker_ids=list(range(copies)), duration_ns=0))
+    trace.total_ns = total
+    logits = runner.logits.view(copies, S * config.segment_size, -1)[:, :n]
+    if return_numpy:
+        logits = logits.float().cpu().numpy()
+    return logits, trace
 
 
 # =========================================================================

@@ -204,3 +204,23 @@ def test_fused_scoring_nll_matches_logits_path():
     diff = (got.double() - want).abs()
     assert float(diff.max()) < 0.05 and float(diff.mean()) < 5e-3
     assert abs(float(got.double().mean() - want.mean())) < 2e-3
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_minibatch_copies_equal_sequential_bitwise(c1, dtype):
+    """Minibatch mode (armt/cli.py:139-153): every copy of the lockstep grouped
+    run reproduces the one-stream sequential run bitwise, state blocks included."""
+    from paper_2506_05229_b200.executors import run_minibatch
+    cfg, _, prep = c1
+    tokens = cli_tokens(cfg, 4 * cfg.segment_size - 5, seed=9)
+    ref_state = MemoryState.fresh(cfg)
+    want, _ = run_sequential(prep[dtype], cfg, tokens, dtype=dtype, state=ref_state)
+    copies = 3
+    st = MemoryState.fresh(cfg, n_layers=copies * cfg.n_layers)
+    got, trace = run_minibatch(prep[dtype], cfg, tokens, copies, dtype=dtype, state=st)
+    assert got.shape == (copies,) + want.shape
+    for b in range(copies):
+        assert np.array_equal(got[b], want)
+        L = cfg.n_layers
+        assert torch.equal(st.A[b * L:(b + 1) * L], ref_state.A)
+    assert trace.steps_executed == 4 * cfg.n_layers
