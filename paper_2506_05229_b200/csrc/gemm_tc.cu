@@ -159,11 +159,17 @@ __device__ __forceinline__ void rope_chunk(float (&x)[CH], const float* cos_col,
 // [4] tiles, [5] epilogue: cycles waiting for a full accumulator, [6] epilogue: total
 __device__ unsigned long long g_gemm_prof[8];
 
-template <int BN, int EPI, int DH, bool PAIR>
+// MC: a 2-CTA cluster of single-CTA MMAs whose two tiles share one operand: the pair
+// (m, n), (m+1, n) shares the B tile and (m, n), (m, n+1) the A tile; each CTA loads
+// its own unshared operand and HALF of the shared one, multicast into both CTAs'
+// smem, so per-CTA L2->SM operand traffic drops by a third with no tile padding.
+template <int BN, int EPI, int DH, bool PAIR, bool MC = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
             const __grid_constant__ Params p) {
   using C = Cfg<BN, PAIR>;
+  constexpr bool CLUSTER = PAIR || MC;
   constexpr int TM = PAIR ? 2 * BM : BM;   // rows per tile (per pair)
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -186,16 +192,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
-  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const uint32_t rank = CLUSTER ? cluster_ctarank() : 0;
+  const int tile0 = CLUSTER ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = CLUSTER ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], MC ? 2 : 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], PAIR ? 8 : 4); }
     for (int i = 0; i < QD; ++i) { mbar_init(&tq_full[i], 1); mbar_init(&tq_empty[i], 5); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -213,12 +219,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
+  if constexpr (CLUSTER) cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles_mn = p.tiles_m * p.tiles_n;
-  const bool dyn = !PAIR && p.tile_ctr != nullptr;
+  const bool dyn = !CLUSTER && p.tile_ctr != nullptr;
+  // tile index -> (member, n-block, m-block); MC: index = pair slot, see the kernel comment
+  bool share_a = false;
+  auto decode = [&](int tile, int& g, int& nb, int& mb) {
+    if constexpr (MC) {
+      const int per_g = (p.tiles_n >> 1) * p.tiles_m;
+      g = tile / per_g;
+      const int rem = tile - g * per_g, j = rem / p.tiles_m, q = rem - j * p.tiles_m;
+      if (q < (p.tiles_m & ~1)) { share_a = false; mb = (q & ~1) + (int)rank; nb = 2 * j + (q & 1); }
+      else { share_a = true; mb = p.tiles_m - 1; nb = 2 * j + (int)rank; }
+    } else {
+      g = tile / tiles_mn;
+      const int r = tile - g * tiles_mn;
+      nb = r / p.tiles_m;
+      mb = r - nb * p.tiles_m;
+    }
+  };
   // consumer side of the queue: entry k (MMA reads every k, epilogue group eg every k = eg mod 2)
   auto tq_pop = [&](int k, bool epi_warp) -> int {
     const int qs = k % QD;
@@ -249,11 +271,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       };
       for (int tile = dyn ? claim() : (tile0 < p.num_tiles ? tile0 : -1); tile >= 0;
            tile = dyn ? claim() : (tile + tstep < p.num_tiles ? tile + tstep : -1)) {
-        const int g = tile / tiles_mn, r = tile - g * tiles_mn;
-        const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
+        int g, nb, mb;
+        decode(tile, g, nb, mb);
         const int a_slot = p.a_slot[g], b_idx = p.b_index[g];
-        const int a_row = p.row0 + mb * TM + (int)rank * BM;
-        const int b_row = nb * BN + (int)rank * C::B_ROWS;
+        const int a_row = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0);
+        const int b_row = nb * BN + (PAIR ? (int)rank * C::B_ROWS : 0);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           if (p.prof) {
             const long long t0 = clock64();
@@ -267,6 +289,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const uint32_t lbar = mapa_shared(&full[stage], 0);
             tma_load_3d_pair(sA + stage * C::A_BYTES, &tmA, lbar, kb * BK, a_row, a_slot);
             tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, lbar, kb * BK, b_row, b_idx);
+          } else if constexpr (MC) {
+            // own operand unicast; half of the shared one multicast to both CTAs
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            if (!share_a) {
+              tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
+              tma_load_3d_mc(sB + stage * C::B_BYTES + rank * (C::B_BYTES / 2), &tmB2, &full[stage], kb * BK,
+                             b_row + (int)rank * (BN / 2), b_idx, (uint16_t)3);
+            } else {
+              tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, b_row, b_idx);
+              tma_load_3d_mc(sA + stage * C::A_BYTES + rank * (C::A_BYTES / 2), &tmA2, &full[stage], kb * BK,
+                             a_row + (int)rank * (BM / 2), a_slot, (uint16_t)3);
+            }
           } else {
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
             tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
@@ -326,6 +360,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             else mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
           }
           if constexpr (PAIR) mma_commit_pair(&empty[stage]);
+          else if constexpr (MC) mma_commit_mc(&empty[stage], (uint16_t)3);  // both CTAs may refill
           else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -350,9 +385,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     auto first = [&]() { const int t = tile0 + eg * tstep; return t < p.num_tiles ? t : -1; };
     for (int tile = dyn ? tq_pop(qk, true) : first(); tile >= 0;
          tile = dyn ? tq_pop(qk += 2, true) : (tile + 2 * tstep < p.num_tiles ? tile + 2 * tstep : -1)) {
-      const int g = tile / tiles_mn, r = tile - g * tiles_mn;
-      const int nb = r / p.tiles_m, mb = r - nb * p.tiles_m;
-      const int row = p.row0 + mb * TM + (int)rank * BM + ew * 32 + lane;
+      int g, nb, mb;
+      decode(tile, g, nb, mb);
+      const int row = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32 + lane;
       const bool live = row < p.M;
       const int c_slot = p.c_slot[g];
       if (p.prof && lane == 0) {
@@ -497,7 +532,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             // (4x fewer L1 wavefronts than row-per-lane 16 B accesses).
             float4* tb = xpose + (warp - 4) * 256;
             const int m4 = lane & 7, rq = lane >> 3;
-            const int wrow0 = p.row0 + mb * TM + (int)rank * BM + ew * 32;
+            const int wrow0 = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32;
             const float* rbase = p.R + (long long)c_slot * p.r_stride;
             float* cbase = reinterpret_cast<float*>(p.C) + (long long)c_slot * p.c_stride;
             __nv_bfloat16* c2base = p.C2 == nullptr ? nullptr : p.C2 + (long long)c_slot * p.c2_stride;
@@ -635,7 +670,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync_all();  // the peer may still read our smem / signal our barriers
+  if constexpr (CLUSTER) cluster_sync_all();  // the peer may still read our smem / signal our barriers
   tc_fence_after();
   if (warp == 2) {
     if constexpr (PAIR)
@@ -682,21 +717,22 @@ static int make_map(CUtensorMap* map, const void* base, long long cols, long lon
   return ARMT_OK;
 }
 
-template <int BN, int EPI, int DH, bool PAIR>
-static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
-  auto kern = gemm_kernel<BN, EPI, DH, PAIR>;
+struct Maps { CUtensorMap a, b, a2, b2; };
+
+template <int BN, int EPI, int DH, bool PAIR, bool MC>
+static int launch(const Maps& m, const Params& p, cudaStream_t s) {
+  auto kern = gemm_kernel<BN, EPI, DH, PAIR, MC>;
   constexpr int smem = (EPI == E_RESIDUAL || EPI == E_RETRIEVE) ? Cfg<BN, PAIR>::SMEM_XPOSE
                                                                  : Cfg<BN, PAIR>::SMEM_BYTES;
   static_assert(smem <= 227 * 1024, "GEMM shared memory budget");
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (PAIR) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr_done = true;
   }
   const int cap = p.max_ctas > 0 && p.max_ctas < num_sms() ? p.max_ctas : num_sms();
-  if constexpr (PAIR) {
-    // one 2-CTA cluster per pair of SMs, persistent over pair tiles
+  if constexpr (PAIR || MC) {
+    // one 2-CTA cluster per pair of SMs, persistent over pair tiles / pair slots
     const int pairs = cap / 2 < 1 ? 1 : cap / 2;
     const int grid = 2 * (p.num_tiles < pairs ? p.num_tiles : pairs);
     cudaLaunchConfig_t cfg;
@@ -712,11 +748,11 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
-    ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 pair gemm launch: %s", cudaGetErrorString(e));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, p);
+    ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 cluster gemm launch: %s", cudaGetErrorString(e));
   } else {
     const int grid = p.num_tiles < cap ? p.num_tiles : cap;
-    kern<<<grid, NUM_THREADS, smem, s>>>(ma, mb, p);
+    kern<<<grid, NUM_THREADS, smem, s>>>(m.a, m.b, m.a2, m.b2, p);
   }
   ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
   return ARMT_OK;
@@ -749,27 +785,27 @@ static int pick_bn(const ArmtGemmArgs& a) {
   return best;
 }
 
-template <int BN, bool PAIR>
-static int dispatch_epi(const ArmtGemmArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+template <int BN, bool PAIR, bool MC>
+static int dispatch_epi(const ArmtGemmArgs& a, const Maps& m, const Params& p,
                         cudaStream_t s) {
   switch (a.epilogue) {
-    case ARMT_EPI_STORE: return launch<BN, E_STORE, 0, PAIR>(ma, mb, p, s);
-    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0, PAIR>(ma, mb, p, s);
-    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0, PAIR>(ma, mb, p, s);
+    case ARMT_EPI_STORE: return launch<BN, E_STORE, 0, PAIR, MC>(m, p, s);
+    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0, PAIR, MC>(m, p, s);
+    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0, PAIR, MC>(m, p, s);
     case ARMT_EPI_LSE:
-      if constexpr (BN == 256) return launch<BN, E_LSE, 0, PAIR>(ma, mb, p, s);
+      if constexpr (BN == 256) return launch<BN, E_LSE, 0, PAIR, MC>(m, p, s);
       break;
     case ARMT_EPI_SWIGLU:
-      if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0, PAIR>(ma, mb, p, s);
+      if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0, PAIR, MC>(m, p, s);
       break;
     case ARMT_EPI_ROPE:
       if constexpr (BN >= 128) {
         switch (a.head_dim) {
-          case 8: return launch<BN, E_ROPE, 8, PAIR>(ma, mb, p, s);
-          case 16: return launch<BN, E_ROPE, 16, PAIR>(ma, mb, p, s);
-          case 32: return launch<BN, E_ROPE, 32, PAIR>(ma, mb, p, s);
-          case 64: return launch<BN, E_ROPE, 64, PAIR>(ma, mb, p, s);
-          case 128: return launch<BN, E_ROPE, 128, PAIR>(ma, mb, p, s);
+          case 8: return launch<BN, E_ROPE, 8, PAIR, MC>(m, p, s);
+          case 16: return launch<BN, E_ROPE, 16, PAIR, MC>(m, p, s);
+          case 32: return launch<BN, E_ROPE, 32, PAIR, MC>(m, p, s);
+          case 64: return launch<BN, E_ROPE, 64, PAIR, MC>(m, p, s);
+          case 128: return launch<BN, E_ROPE, 128, PAIR, MC>(m, p, s);
           default: break;
         }
       }
@@ -788,18 +824,27 @@ int make_tma_map_bf16(CUtensorMap* map, const void* base, long long cols, long l
 
 // One launch over rows [row0, m_end) of every member; pair = CTA-pair (2-CTA) tiles.
 static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_end, cudaStream_t s,
-                     int max_ctas = -1) {
+                     int max_ctas = -1, bool mc = false) {
   using namespace tc;
   int max_a = 0, max_b = 0;
   for (int g = 0; g < a.G; ++g) {
     max_a = a.a_slot[g] > max_a ? a.a_slot[g] : max_a;
     max_b = a.b_index[g] > max_b ? a.b_index[g] : max_b;
   }
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM);
+  Maps maps;
+  int rc = make_map(&maps.a, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM);
   if (rc) return rc;
-  rc = make_map(&mb, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, pair ? bn / 2 : bn);
+  rc = make_map(&maps.b, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, pair ? bn / 2 : bn);
   if (rc) return rc;
+  if (mc) {   // half-tile boxes for the multicast halves of the shared operand
+    rc = make_map(&maps.a2, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM / 2);
+    if (rc) return rc;
+    rc = make_map(&maps.b2, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, bn / 2);
+    if (rc) return rc;
+  } else {
+    maps.a2 = maps.a;
+    maps.b2 = maps.b;
+  }
 
   Params p;
   memset(&p, 0, sizeof(p));
@@ -807,7 +852,7 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.G = a.G; p.M = m_end; p.N = a.N; p.K = a.K; p.row0 = row0;
   p.tiles_m = (m_end - row0 + tm - 1) / tm;
   p.tiles_n = (a.N + bn - 1) / bn;
-  p.num_tiles = a.G * p.tiles_m * p.tiles_n;
+  p.num_tiles = mc ? a.G * (p.tiles_n / 2) * p.tiles_m : a.G * p.tiles_m * p.tiles_n;
   p.k_blocks = (a.K + BK - 1) / BK;
   p.c_dtype = a.c_dtype;
   p.C = a.C; p.ldc = a.ldc; p.c_stride = a.c_stride;
@@ -823,7 +868,7 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.rope_ld = a.M;  // tables are (head_dim/2, M): one column per position of the full member
   p.swiglu_block = a.swiglu_block;
   p.max_ctas = max_ctas >= 0 ? max_ctas : a.max_ctas;
-  if (!pair) {
+  if (!pair && !mc) {
     // dynamic tile scheduling: a fresh {next, done} counter pair per launch from a ring in
     // device memory (each launch's last CTA re-zeroes its pair, so graph replays reuse it)
     static int* ring = nullptr;
@@ -870,9 +915,12 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     p.c_slot[g] = (short)a.c_slot[g];
   }
   switch (bn) {
-    case 64: return dispatch_epi<64, false>(a, ma, mb, p, s);
-    case 128: return dispatch_epi<128, false>(a, ma, mb, p, s);
-    case 256: return pair ? dispatch_epi<256, true>(a, ma, mb, p, s) : dispatch_epi<256, false>(a, ma, mb, p, s);
+    case 64: return dispatch_epi<64, false, false>(a, maps, p, s);
+    case 128: return dispatch_epi<128, false, false>(a, maps, p, s);
+    case 256:
+      if (pair) return dispatch_epi<256, true, false>(a, maps, p, s);
+      if (mc) return dispatch_epi<256, false, true>(a, maps, p, s);
+      return dispatch_epi<256, false, false>(a, maps, p, s);
   }
   return ARMT_ERR_UNSUPPORTED;
 }
@@ -902,7 +950,14 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   const bool conc = (pe && strcmp(pe, "conc") == 0) || (!pe && a.epilogue == ARMT_EPI_ROPE);
   const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) &&
                     a.K >= (heavy_epi ? 4096 : 1024) && !(pe && pe[0] == '0');
-  if (!pair) return gemm_rows(a, bn, false, 0, a.M, s);
+  if (!pair) {
+    // multicast clusters (ARMT_GEMM_MC=0 disables): 256-wide tiles, an even number of
+    // n-blocks (pair slots), mainloop-heavy shapes
+    const char* me = getenv("ARMT_GEMM_MC");
+    const int tiles_n = (a.N + bn - 1) / bn;
+    const bool mc = bn == 256 && (tiles_n % 2 == 0) && a.K >= 1024 && !(me && me[0] == '0') && a.max_ctas == 0;
+    return gemm_rows(a, bn, false, 0, a.M, s, -1, mc);
+  }
   if (m_pair == a.M) return gemm_rows(a, bn, true, 0, m_pair, s);
   if (!conc) {
     int rc = gemm_rows(a, bn, true, 0, m_pair, s);

@@ -296,21 +296,24 @@ def test_logits_nll_matches_log_softmax(dtype, V):
 
 
 @pytest.mark.parametrize("epi", ["store", "residual", "rope", "swiglu", "lse"])
-def test_tc_gemm_cta_pair_matches_single_cta(epi, monkeypatch):
+def test_tc_gemm_cta_pair_and_multicast_match_single_cta(epi, monkeypatch):
     """The CTA-pair (cta_group::2, 256-row) tiles plus the single-CTA remainder
-    launch must reproduce the single-CTA kernel at a C2 member height (1152
-    rows = 4 pair tiles + 128 remainder rows) for every epilogue."""
+    launch, and the multicast clusters (B- or A-sharing tile pairs), must
+    reproduce the plain single-CTA kernel at a C2 member height (1152 rows = 4
+    pair tiles + 128 remainder rows; 9 m-tiles = 4 B-sharing pairs + 1
+    A-sharing pair per n-block pair) for every epilogue."""
     torch.manual_seed(7)
     G, M = 3, 1152
     K = 4096 if epi == "residual" else 1024
-    dh, H = 64, 4
+    dh, H = 64, 8
     N = {"store": 512, "residual": 512, "rope": 3 * H * dh, "swiglu": 1024, "lse": 1000}[epi]
     A = torch.randn(G, M, K, device=DEV).bfloat16()
     B = (torch.randn(G, N, K, device=DEV) * 0.05).bfloat16()
     monkeypatch.setenv("ARMT_GEMM_BN", "256")
 
-    def run(pair):
+    def run(pair, mc="0"):
         monkeypatch.setenv("ARMT_GEMM_PAIR", pair)
+        monkeypatch.setenv("ARMT_GEMM_MC", mc)
         kw, outs = {}, []
         if epi == "store":
             C = torch.zeros(G, M, N, device=DEV)
@@ -354,7 +357,8 @@ def test_tc_gemm_cta_pair_matches_single_cta(epi, monkeypatch):
         torch.cuda.synchronize()
         return [o.float().clone() for o in outs]
 
-    single, paired = run("0"), run("1")
-    for s_, p_ in zip(single, paired):
+    single, paired, multicast = run("0"), run("split"), run("0", "1")
+    for s_, p_, m_ in zip(single, paired, multicast):
         assert torch.isfinite(p_).all()
         assert rel(p_, s_) < 1e-6, (epi, rel(p_, s_))
+        assert torch.equal(m_, s_), (epi, rel(m_, s_))   # same MMA per tile: bitwise
