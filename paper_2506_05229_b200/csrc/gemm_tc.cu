@@ -325,7 +325,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (lane == 0 && (!PAIR || rank == 0)) {
       // ---------------- MMA issuer (single thread; the pair leader in PAIR mode)
       constexpr uint32_t idesc = instr_desc<TM, BN>();
       int stage = 0; uint32_t phase = 0;

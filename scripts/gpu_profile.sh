@@ -14,5 +14,5 @@ timeout 600 $NCU --set full --import-source on -k regex:gemm_kernel -s 6 -c 2 -o
   python scripts/kernel_bench.py --G 16 --ops qkv --iters 1 > gpurun_out/full_qkv.log 2>&1
 timeout 600 $NCU --set full --import-source on -k regex:attn -s 3 -c 1 -o gpurun_out/full_attn \
   python scripts/kernel_bench.py --G 16 --ops attn --iters 1 > gpurun_out/full_attn.log 2>&1
-timeout 600 $NCU --set full --import-source on -k regex:fold -s 12 -c 3 -o gpurun_out/full_fold \
+timeout 600 $NCU --set full --import-source on -k regex:fold -s 3 -c 3 -o gpurun_out/full_fold \
   python scripts/kernel_bench.py --G 16 --ops foldtc --iters 1 > gpurun_out/full_fold.log 2>&1

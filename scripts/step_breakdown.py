@@ -10,6 +10,9 @@ import json
 import os
 import sys
 
+# per-op events are recorded on the current stream: time the one-stream issue order
+os.environ.setdefault("ARMT_DUAL", "0")
+
 import numpy as np
 import torch
 
