@@ -270,9 +270,10 @@ __global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__
 // blocks: off-diagonal update from finished rows (L row block read as float4
 // broadcasts), then in-block forward substitution in registers. Output U^T as
 // the [hi | hi | lo] bf16x3 A operand of GEMM3.
-// Two columns per thread (n and n + 128): every LT broadcast load feeds 2x16 FMAs.
+// One column per thread, 256 threads: 8 warps per SM hide the shared-memory
+// latency of the substitution (the 2-columns-per-thread, 4-warp form was 73 us at C2).
 constexpr int SOLVE_COLS = 256;
-__global__ void __launch_bounds__(128) fold_solve_kernel(const float* __restrict__ kvb, long long ld_kvb,
+__global__ void __launch_bounds__(256) fold_solve_kernel(const float* __restrict__ kvb, long long ld_kvb,
                                                          long long kvb_stride, int v_off, Geom q, Ws w) {
   extern __shared__ __align__(16) float sm[];
   const int Mp = q.Mp, M = q.M;
@@ -281,63 +282,54 @@ __global__ void __launch_bounds__(128) fold_solve_kernel(const float* __restrict
   float* us = LT + Mp * Mp;           // [Mp][US]
   const int g = blockIdx.y;
   const int n0 = blockIdx.x * SOLVE_COLS;
-  const int c0 = threadIdx.x, c1 = threadIdx.x + 128;
-  const bool live0 = n0 + c0 < q.d, live1 = n0 + c1 < q.d;
+  const int c0 = threadIdx.x;
+  const bool live0 = n0 + c0 < q.d;
   const float4* Lg = reinterpret_cast<const float4*>(w.L + (long long)g * Mp * Mp);  // already LT layout
   for (int e = threadIdx.x; e < Mp * Mp / 4; e += blockDim.x) reinterpret_cast<float4*>(LT)[e] = Lg[e];
   const float* beta = w.beta + (long long)g * Mp;
   const float* coef = w.coef + (long long)g * Mp;
   const float* Pf = w.Pf + (long long)g * M * q.NP1;
   const float* kv = kvb + (long long)g * kvb_stride;
-  for (int i0 = 0; i0 < Mp; i0 += 8) {  // 32 independent loads in flight per thread
-    float v0[8], p0[8], v1[8], p1[8];
+  for (int i0 = 0; i0 < Mp; i0 += 16) {  // 32 independent loads in flight per thread
+    float v0[16], p0[16];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < 16; ++t) {
       const int i = i0 + t;
-      const bool ok = i < M;
-      v0[t] = (ok && live0) ? kv[(long long)i * ld_kvb + v_off + n0 + c0] : 0.f;
-      p0[t] = (ok && live0) ? Pf[(long long)i * q.NP1 + n0 + c0] : 0.f;
-      v1[t] = (ok && live1) ? kv[(long long)i * ld_kvb + v_off + n0 + c1] : 0.f;
-      p1[t] = (ok && live1) ? Pf[(long long)i * q.NP1 + n0 + c1] : 0.f;
+      const bool ok = i < M && live0;
+      v0[t] = ok ? kv[(long long)i * ld_kvb + v_off + n0 + c0] : 0.f;
+      p0[t] = ok ? Pf[(long long)i * q.NP1 + n0 + c0] : 0.f;
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      us[(i0 + t) * US + c0] = beta[i0 + t] * v0[t] - coef[i0 + t] * p0[t];
-      us[(i0 + t) * US + c1] = beta[i0 + t] * v1[t] - coef[i0 + t] * p1[t];
-    }
+    for (int t = 0; t < 16; ++t) us[(i0 + t) * US + c0] = beta[i0 + t] * v0[t] - coef[i0 + t] * p0[t];
   }
   __syncthreads();
   for (int b = 0; b < Mp; b += 16) {
-    float x[16], y[16];
+    float x[16];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) { x[t] = us[(b + t) * US + c0]; y[t] = us[(b + t) * US + c1]; }
+    for (int t = 0; t < 16; ++t) x[t] = us[(b + t) * US + c0];
     for (int j = 0; j < b; ++j) {
-      const float u0 = us[j * US + c0], u1 = us[j * US + c1];
+      const float u0 = us[j * US + c0];
       const float4* lrow = reinterpret_cast<const float4*>(LT + j * Mp + b);
 #pragma unroll
       for (int t4 = 0; t4 < 4; ++t4) {
         const float4 l = lrow[t4];
-        x[4 * t4 + 0] = fmaf(-l.x, u0, x[4 * t4 + 0]); y[4 * t4 + 0] = fmaf(-l.x, u1, y[4 * t4 + 0]);
-        x[4 * t4 + 1] = fmaf(-l.y, u0, x[4 * t4 + 1]); y[4 * t4 + 1] = fmaf(-l.y, u1, y[4 * t4 + 1]);
-        x[4 * t4 + 2] = fmaf(-l.z, u0, x[4 * t4 + 2]); y[4 * t4 + 2] = fmaf(-l.z, u1, y[4 * t4 + 2]);
-        x[4 * t4 + 3] = fmaf(-l.w, u0, x[4 * t4 + 3]); y[4 * t4 + 3] = fmaf(-l.w, u1, y[4 * t4 + 3]);
+        x[4 * t4 + 0] = fmaf(-l.x, u0, x[4 * t4 + 0]);
+        x[4 * t4 + 1] = fmaf(-l.y, u0, x[4 * t4 + 1]);
+        x[4 * t4 + 2] = fmaf(-l.z, u0, x[4 * t4 + 2]);
+        x[4 * t4 + 3] = fmaf(-l.w, u0, x[4 * t4 + 3]);
       }
     }
 #pragma unroll
     for (int t = 1; t < 16; ++t)
 #pragma unroll
-      for (int s = 0; s < t; ++s) {
-        const float l = LT[(b + s) * Mp + b + t];
-        x[t] = fmaf(-l, x[s], x[t]);
-        y[t] = fmaf(-l, y[s], y[t]);
-      }
+      for (int s = 0; s < t; ++s) x[t] = fmaf(-LT[(b + s) * Mp + b + t], x[s], x[t]);
 #pragma unroll
-    for (int t = 0; t < 16; ++t) { us[(b + t) * US + c0] = x[t]; us[(b + t) * US + c1] = y[t]; }
+    for (int t = 0; t < 16; ++t) us[(b + t) * US + c0] = x[t];
   }
   __syncthreads();
-  // U^T rows [hi | hi | lo]: warp w writes rows n0 + w, n0 + w + 4, ...; lanes walk tokens
+  // U^T rows [hi | hi | lo]: warp w writes rows n0 + w, n0 + w + 8, ...; lanes walk tokens
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rr = warp; rr < SOLVE_COLS; rr += 4) {
+  for (int rr = warp; rr < SOLVE_COLS; rr += 8) {
     if (n0 + rr >= q.d) break;
     __nv_bfloat16* out = w.UTs + ((long long)g * q.d + n0 + rr) * 3 * Mp;
     for (int i = 2 * lane; i < Mp; i += 64) {
@@ -413,7 +405,7 @@ extern "C" int armt_mem_fold_tc(const ArmtMembers* mem, const float* kvb, long l
   ARMT_REQUIRE(solve_smem <= 227 * 1024, ARMT_ERR_UNSUPPORTED, "fold_tc: M too large for the solve");
   cudaFuncSetAttribute(fold_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem);
   dim3 grid((d + SOLVE_COLS - 1) / SOLVE_COLS, mem->G);
-  fold_solve_kernel<<<grid, 128, solve_smem, s>>>(kvb, ld_kvb, kvb_stride, v_off, q, w);
+  fold_solve_kernel<<<grid, SOLVE_COLS, solve_smem, s>>>(kvb, ld_kvb, kvb_stride, v_off, q, w);
   ARMT_CHECK_LAUNCH("fold_solve");
 
   // GEMM3: A[layer] = A[layer] + U^T Phi (d x dphi, K = 3Mp); memop rows [0, d) <- split(A)
