@@ -65,18 +65,24 @@ def launches(path):
 
 
 def full_metrics(rep):
+    """Key metrics of every kernel in a --set full report (one dict per launch)."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, v = rows[0], rows[2] if len(rows) > 2 else rows[1]
-    res = {"kernel": short(v[h.index("Kernel Name")]) if "Kernel Name" in h else ""}
-    for key, m in METRICS.items():
-        if m in h:
-            try:
-                res[key] = float(v[h.index(m)].replace(",", ""))
-            except ValueError:
-                res[key] = v[h.index(m)]
-    return res
+    h = rows[0]
+    res_all = []
+    for v in rows[2:] if len(rows) > 2 else rows[1:]:
+        if len(v) != len(h):
+            continue
+        res = {"kernel": short(v[h.index("Kernel Name")]) if "Kernel Name" in h else ""}
+        for key, m in METRICS.items():
+            if m in h:
+                try:
+                    res[key] = float(v[h.index(m)].replace(",", ""))
+                except ValueError:
+                    res[key] = v[h.index(m)]
+        res_all.append(res)
+    return res_all
 
 
 def main():
@@ -85,8 +91,9 @@ def main():
     ap.add_argument("--full", action="append", default=[])
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--note", default="")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles"))
     args = ap.parse_args()
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    os.makedirs(args.out, exist_ok=True)
     if args.launches:
         agg = launches(args.launches)
         tot = sum(v[1] for v in agg.values())
@@ -95,13 +102,14 @@ def main():
                  "| share | total ms | launches | avg us | kernel |", "|---:|---:|---:|---:|---|"]
         for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
             lines.append(f"| {v / tot * 100:.1f}% | {v / 1e6:.3f} | {n} | {v / n / 1e3:.1f} | `{k}` |")
-        open(os.path.join(ROOT, "profiles", f"{args.tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+        open(os.path.join(args.out, f"{args.tag}_launches.md"), "w").write("\n".join(lines) + "\n")
     if args.full:
         res = {}
         for item in args.full:
             label, rep = item.split("=", 1)
-            res[label] = full_metrics(rep)
-        json.dump(res, open(os.path.join(ROOT, "profiles", f"{args.tag}_kernels.json"), "w"), indent=1)
+            for k, m in enumerate(full_metrics(rep)):
+                res[label if k == 0 else f"{label}.{k}"] = m
+        json.dump(res, open(os.path.join(args.out, f"{args.tag}_kernels.json"), "w"), indent=1)
         lines = [f"# {args.tag}: ncu --set full captures (one launch each)", "", args.note, "",
                  "| capture | kernel | us | DRAM MB (r+w) | tensor % | L2 % | DRAM % | issue % | regs |",
                  "|---|---|---:|---:|---:|---:|---:|---:|---:|"]
@@ -111,7 +119,7 @@ def main():
                          f"{m.get('tensor_pipe_pct', 0):.1f} | {m.get('l2_throughput_pct', 0):.1f} | "
                          f"{m.get('dram_throughput_pct', 0):.1f} | {m.get('issue_active_pct', 0):.1f} | "
                          f"{m.get('registers', 0):.0f} |")
-        open(os.path.join(ROOT, "profiles", f"{args.tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+        open(os.path.join(args.out, f"{args.tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
