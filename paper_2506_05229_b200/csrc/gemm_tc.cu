@@ -56,6 +56,7 @@ struct Params {
   int pf, pf_a;  // L2 prefetch distance in k-blocks for B (and A) tiles; 0 = off
   int row0;    // first row of every member this launch covers (rows [row0, M))
   int* tile_ctr;  // dynamic tile scheduling: {next tile, CTAs done} for this launch (nullptr = static)
+  int cst;     // bf16 outputs stored through the smem transpose (coalesced 64 B row segments)
   int xpose;   // residual/retrieve epilogue through the smem transpose (coalesced 128 B rows)
   int prof;    // ARMT_GEMM_PROF=1: accumulate wait cycles of the producer / MMA issuer
   short a_slot[ARMT_MAX_MEMBERS];
@@ -133,6 +134,29 @@ __device__ __forceinline__ void load_row32_f32(const float* p, int cnt, bool vec
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = j < cnt ? p[j] : 0.f;
   }
+}
+
+// Coalesced bf16 store of a 32-row x 32-column chunk held row-per-lane (lane = row
+// wrow0 + lane): bf16 rows go through a 64 B-per-row swizzled smem tile (2 KB per warp)
+// and leave as 16 B per lane with 4 lanes per row segment, so each store instruction
+// writes 8 full 64 B row segments instead of 32 scattered 16 B pieces.
+__device__ __forceinline__ void store_chunk_bf16_coalesced(uint4* tb, int lane, const float (&v)[32],
+                                                           __nv_bfloat16* base, long long ld, int wrow0,
+                                                           int M, int col0) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    tb[lane * 4 + (c ^ ((lane >> 1) & 3))] =
+        make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                   pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+  __syncwarp();
+  const int c = lane & 3;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = (lane >> 2) + 8 * k;
+    const uint4 val = tb[r * 4 + (c ^ ((r >> 1) & 3))];
+    if (wrow0 + r < M) *reinterpret_cast<uint4*>(base + (long long)(wrow0 + r) * ld + col0 + 8 * c) = val;
+  }
+  __syncwarp();
 }
 
 // RoPE over one chunk of CH (>= DH, multiple of DH) columns held in registers.
@@ -468,7 +492,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const float gv = gte[j] * rs;
             gte[j] = gv * __frcp_rn(1.f + __expf(-gv)) * (up[j] * rs);
           }
-          if (live && out_n0 + c0 < p.N / 2) store_row32(p.C, ARMT_BF16, off, out_n0 + c0, p.N / 2, p.ldc, gte);
+          if (p.cst && out_n0 + c0 + 32 <= p.N / 2) {
+            store_chunk_bf16_coalesced(reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128, lane, gte,
+                                       reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride,
+                                       p.ldc, row - lane, p.M, out_n0 + c0);
+          } else if (live && out_n0 + c0 < p.N / 2) {
+            store_row32(p.C, ARMT_BF16, off, out_n0 + c0, p.N / 2, p.ldc, gte);
+          }
         }
       } else if constexpr (EPI == E_ROPE) {
         // tables are (DH/2, M) column-major in position: lane = row reads consecutive words
@@ -500,6 +530,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     x2[j] = b * cs + a * sn;
                   }
                 }
+                if (!p.cst) {
+                  store_row32(p.C, ARMT_BF16, off, n0 + 32 * q, p.N, p.ldc, x1);
+                  store_row32(p.C, ARMT_BF16, off, n0 + DH / 2 + 32 * q, p.N, p.ldc, x2);
+                }
+              }
+              if (p.cst && n0 + DH <= p.N) {  // (warp-uniform: every lane stores through smem)
+                uint4* tb = reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128;
+                __nv_bfloat16* cb = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride;
+                store_chunk_bf16_coalesced(tb, lane, x1, cb, p.ldc, row - lane, p.M, n0 + 32 * q);
+                store_chunk_bf16_coalesced(tb, lane, x2, cb, p.ldc, row - lane, p.M, n0 + DH / 2 + 32 * q);
+              } else if (p.cst && live && n0 < p.N) {
                 store_row32(p.C, ARMT_BF16, off, n0 + 32 * q, p.N, p.ldc, x1);
                 store_row32(p.C, ARMT_BF16, off, n0 + DH / 2 + 32 * q, p.N, p.ldc, x2);
               }
@@ -613,6 +654,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           __syncwarp();
           tmem_ld32(tbase + c0, v);
           const int n0 = nb * BN + c0;
+          if constexpr (EPI == E_STORE) {
+            if (p.cst && p.c_dtype == ARMT_BF16 && n0 + 32 <= p.N) {  // warp-uniform
+              store_chunk_bf16_coalesced(reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128, lane, v,
+                                         reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride,
+                                         p.ldc, row - lane, p.M, n0);
+              continue;
+            }
+          }
           if (!live || n0 >= p.N) continue;  // after the warp-wide load: safe
           if constexpr (EPI == E_RESIDUAL || EPI == E_RETRIEVE) {
             const float* rp = p.R + (long long)c_slot * p.r_stride + (long long)row * p.ldr + n0;
@@ -722,8 +771,7 @@ struct Maps { CUtensorMap a, b, a2, b2; };
 template <int BN, int EPI, int DH, bool PAIR, bool MC>
 static int launch(const Maps& m, const Params& p, cudaStream_t s) {
   auto kern = gemm_kernel<BN, EPI, DH, PAIR, MC>;
-  constexpr int smem = (EPI == E_RESIDUAL || EPI == E_RETRIEVE) ? Cfg<BN, PAIR>::SMEM_XPOSE
-                                                                 : Cfg<BN, PAIR>::SMEM_BYTES;
+  constexpr int smem = (EPI == E_LSE) ? Cfg<BN, PAIR>::SMEM_BYTES : Cfg<BN, PAIR>::SMEM_XPOSE;
   static_assert(smem <= 227 * 1024, "GEMM shared memory budget");
   static bool attr_done = false;
   if (!attr_done) {
@@ -898,6 +946,10 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
                                          reinterpret_cast<uintptr_t>(a.C2) % 8 == 0)) &&
                     (a.c_stride % 4 == 0) && (a.r_stride % 4 == 0) && (a.C2 == nullptr || a.c2_stride % 4 == 0);
     p.xpose = al && !(xe && xe[0] == '0') ? 1 : 0;
+    const char* ce = getenv("ARMT_GEMM_CST");
+    p.cst = (a.c_dtype == ARMT_BF16 || a.epilogue == ARMT_EPI_SWIGLU || a.epilogue == ARMT_EPI_ROPE) &&
+            a.ldc % 8 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 && a.c_stride % 8 == 0 &&
+            !(ce && ce[0] == '0') ? 1 : 0;
   }
   {
     const char* f = getenv("ARMT_GEMM_PF");
