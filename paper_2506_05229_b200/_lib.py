@@ -14,7 +14,8 @@ import os
 from .errors import DeviceError, DimensionError, InputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libarmt_b200.so")
+# ARMT_LIB_PATH: load an experimental build of the same C-ABI (A/B runs)
+LIB_PATH = os.environ.get("ARMT_LIB_PATH") or os.path.join(HERE, "libarmt_b200.so")
 
 MAX_MEMBERS = 128
 F32, BF16 = 0, 1
