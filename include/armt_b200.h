@@ -47,9 +47,12 @@ typedef enum {
   ARMT_EPI_RETRIEVE = 2,  /* C = R + (|den| <= eps ? 0 : acc/den)  armt/memory.py:149-152 */
   ARMT_EPI_SWIGLU = 3,    /* C[:, j] = silu(acc_gate) * acc_up     armt/layers.py:228-232 */
   ARMT_EPI_ROPE = 4,      /* C = rope(acc) on cols < rope_cols     armt/layers.py:169-176 */
-  ARMT_EPI_LSE = 5        /* no C: per row and N-tile (max, sum exp) of acc in base-2 units into
+  ARMT_EPI_LSE = 5,       /* no C: per row and N-tile (max, sum exp) of acc in base-2 units into
                              lse_part[row*lse_ld + nb] (float2), and acc[row][targets[row]] into
                              lse_tgt[row] -- the fused next-token NLL of the LM head */
+  ARMT_EPI_DPFP = 6       /* acc = q (M x N, N = d_mem <= 64): C = bf16 DPFP_nu(q) (ldc >= 2*nu*N) and
+                             den[g*den_stride + m] = DPFP(q) . z[e_index[g]] (z rows of 2*nu*N floats)
+                             armt/memory.py:34-45,137-147 -- retrieval's feature map fused into q-proj */
 } ArmtEpilogue;
 
 /* Members of one grouped launch: member g runs slot[g] against layer[g]. */
@@ -89,9 +92,11 @@ typedef struct {
   int swiglu_block;                     /* SWIGLU: cols [t*2b, t*2b+b) gate, [t*2b+b, (t+1)*2b) up */
   int max_ctas;                         /* bf16 engine: cap on resident CTAs (0 = one per SM); lets a
                                            launch leave SMs free for a concurrent stream */
+  const float* z; int nu;               /* DPFP: memory normaliser rows and feature-map order */
   int a_slot[ARMT_MAX_MEMBERS];
   int b_index[ARMT_MAX_MEMBERS];
   int c_slot[ARMT_MAX_MEMBERS];
+  int e_index[ARMT_MAX_MEMBERS];        /* DPFP: memory-state row of member g's z */
 } ArmtGemmArgs;
 
 /* Replaces grouped_gemm / gemm / _project (armt/tensor_ops.py:204-264,

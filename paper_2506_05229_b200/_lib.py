@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("ARMT_LIB_PATH") or os.path.join(HERE, "libarmt_b200.s
 
 MAX_MEMBERS = 128
 F32, BF16 = 0, 1
-EPI_STORE, EPI_RESIDUAL, EPI_RETRIEVE, EPI_SWIGLU, EPI_ROPE, EPI_LSE = 0, 1, 2, 3, 4, 5
+EPI_STORE, EPI_RESIDUAL, EPI_RETRIEVE, EPI_SWIGLU, EPI_ROPE, EPI_LSE, EPI_DPFP = 0, 1, 2, 3, 4, 5, 6
 
 # Every symbol the header declares (checked by tests/test_boundary.py).
 EXPORTS = ("armt_gemm", "armt_embed", "armt_rmsnorm", "armt_dpfp_den", "armt_attention",
@@ -58,9 +58,11 @@ class ArmtGemmArgs(ctypes.Structure):
         ("head_dim", _I), ("rope_cols", _I),
         ("swiglu_block", _I),
         ("max_ctas", _I),
+        ("z", _P), ("nu", _I),
         ("a_slot", _I * MAX_MEMBERS),
         ("b_index", _I * MAX_MEMBERS),
         ("c_slot", _I * MAX_MEMBERS),
+        ("e_index", _I * MAX_MEMBERS),
     ]
 
 

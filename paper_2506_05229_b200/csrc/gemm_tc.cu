@@ -62,6 +62,8 @@ struct Params {
   short a_slot[ARMT_MAX_MEMBERS];
   short b_index[ARMT_MAX_MEMBERS];
   short c_slot[ARMT_MAX_MEMBERS];
+  short e_index[ARMT_MAX_MEMBERS];
+  const float* z; int nu;
 };
 
 // PAIR: a 2-CTA cluster computes a 256 x BN tile with one cta_group::2 MMA per K
@@ -83,7 +85,7 @@ template <int BN, bool PAIR = false> struct Cfg {
 using namespace tcx;
 
 // ---------------------------------------------------------------- epilogues
-enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4, E_LSE = 5 };
+enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4, E_LSE = 5, E_DPFP = 6 };
 
 __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = 0
   float y;
@@ -449,7 +451,47 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       }
 
-      if constexpr (EPI == E_LSE) {
+      if constexpr (EPI == E_DPFP) {
+        // acc row = q (d_mem = DH <= 64 columns): phi = DPFP_nu(q) straight to bf16 (the
+        // retrieval numerator's A operand) and den = phi . z[layer], one row per thread
+        // (armt/memory.py:34-45,137-147); replaces the q f32 round trip + a separate kernel
+        static_assert(DH >= 8 && DH <= 64, "DPFP epilogue: d_mem in [8, 64]");
+        float qv[64];
+        __syncwarp();
+        tmem_ld32(tbase, *reinterpret_cast<float(*)[32]>(qv));
+        if constexpr (DH > 32) {
+          __syncwarp();
+          tmem_ld32(tbase + 32, *reinterpret_cast<float(*)[32]>(qv + 32));
+        }
+        const float* zr = p.z + (long long)p.e_index[g] * (2 * DH * p.nu);
+        __nv_bfloat16* cb = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride;
+        uint4* tb = reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128;
+        float dacc = 0.f;
+        auto rv = [&](int i) { return i < DH ? fmaxf(qv[i], 0.f) : fmaxf(-qv[i - DH], 0.f); };
+#pragma unroll
+        for (int j = 1; j <= 3; ++j) {
+          if (j > p.nu) break;  // warp-uniform
+#pragma unroll
+          for (int c0 = 0; c0 < 2 * DH; c0 += 32) {
+            float ph[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const int i = c0 + t;
+              ph[t] = (i < 2 * DH) ? rv(i) * rv((i + j) % (2 * DH)) : 0.f;
+            }
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (c0 + t < 2 * DH) dacc = fmaf(ph[t], zr[(j - 1) * 2 * DH + c0 + t], dacc);
+            const int col0 = (j - 1) * 2 * DH + c0;
+            if constexpr ((2 * DH) % 32 == 0) {
+              store_chunk_bf16_coalesced(tb, lane, ph, cb, p.ldc, row - lane, p.M, col0);
+            } else {
+              if (live) store_row32(p.C, ARMT_BF16, off, col0, col0 + min(32, 2 * DH - c0), p.ldc, ph);
+            }
+          }
+        }
+        if (live) const_cast<float*>(p.den)[(long long)g * p.den_stride + row] = dacc;  // (RETRIEVE reads den)
+      } else if constexpr (EPI == E_LSE) {
         // fused next-token NLL: online (max, sum 2^x) of the row's logits in base 2
         constexpr float LOG2E = 1.4426950408889634f;
         float m = -INFINITY, ssum = 0.f, tv = 0.f;
@@ -809,6 +851,7 @@ static int launch(const Maps& m, const Params& p, cudaStream_t s) {
 static int pick_bn(const ArmtGemmArgs& a) {
   if (a.epilogue == ARMT_EPI_SWIGLU) return 2 * a.swiglu_block;
   if (a.epilogue == ARMT_EPI_LSE) return 256;  // lse_ld = ceil(N / 256) partials per row
+  if (a.epilogue == ARMT_EPI_DPFP) return 64;  // one tile holds a whole q row
   if (const char* f = getenv("ARMT_GEMM_BN")) {  // tests: force a tile width
     const int v = atoi(f);
     if ((v == 64 || v == 128 || v == 256) && (a.epilogue != ARMT_EPI_ROPE || (v >= 128 && v % a.head_dim == 0)))
@@ -842,6 +885,16 @@ static int dispatch_epi(const ArmtGemmArgs& a, const Maps& m, const Params& p,
     case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0, PAIR, MC>(m, p, s);
     case ARMT_EPI_LSE:
       if constexpr (BN == 256) return launch<BN, E_LSE, 0, PAIR, MC>(m, p, s);
+      break;
+    case ARMT_EPI_DPFP:
+      if constexpr (BN == 64 && !PAIR && !MC) {
+        switch (a.N) {
+          case 16: return launch<BN, E_DPFP, 16, false, false>(m, p, s);
+          case 32: return launch<BN, E_DPFP, 32, false, false>(m, p, s);
+          case 64: return launch<BN, E_DPFP, 64, false, false>(m, p, s);
+          default: break;
+        }
+      }
       break;
     case ARMT_EPI_SWIGLU:
       if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0, PAIR, MC>(m, p, s);
@@ -965,7 +1018,9 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     p.a_slot[g] = (short)a.a_slot[g];
     p.b_index[g] = (short)a.b_index[g];
     p.c_slot[g] = (short)a.c_slot[g];
+    p.e_index[g] = (short)a.e_index[g];
   }
+  p.z = a.z; p.nu = a.nu;
   switch (bn) {
     case 64: return dispatch_epi<64, false, false>(a, maps, p, s);
     case 128: return dispatch_epi<128, false, false>(a, maps, p, s);
@@ -983,6 +1038,10 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   if (a.epilogue == ARMT_EPI_SWIGLU)
     ARMT_REQUIRE((a.swiglu_block == 32 || a.swiglu_block == 128) && a.N % (2 * a.swiglu_block) == 0,
                  ARMT_ERR_UNSUPPORTED, "SwiGLU block must be 32 or 128 and divide N/2");
+  if (a.epilogue == ARMT_EPI_DPFP)
+    ARMT_REQUIRE((a.N == 16 || a.N == 32 || a.N == 64) && a.nu >= 1 && a.nu <= 3 && a.z != nullptr &&
+                 a.den != nullptr && a.ldc >= 2LL * a.nu * a.N && a.ldc % 8 == 0 && a.c_dtype == ARMT_BF16,
+                 ARMT_ERR_UNSUPPORTED, "DPFP epilogue: d_mem in {16,32,64}, nu in [1,3], bf16 phi, ldc %% 8");
   const int bn = tc::pick_bn(a);
   // CTA-pair (cta_group::2, 256-row tiles) for mainloop-bound 256-wide GEMMs: rows
   // [0, 256*floor(M/256)) as pair tiles, the remainder as single-CTA tiles (no padded

@@ -38,6 +38,10 @@ from .errors import DimensionError, InputError
 from .weights import GroupedWeights, expected_shapes
 
 
+# bf16 path: DPFP + phi.z fused into the q-projection epilogue (ARMT_FUSED_DPFP=0: two launches)
+FUSED_DPFP = __import__("os").environ.get("ARMT_FUSED_DPFP", "1") == "1"
+
+
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -365,20 +369,37 @@ class Engine:
         gid = list(range(G))
         src = self.xs_bf if self.bf16 else self.xs
 
-        def fill_q(a):
-            a.M, a.N, a.K, a.ab_dtype = T, cfg.d_mem, d, p.ab
-            a.A, a.lda, a.a_stride = src.data_ptr(), d, T * d
-            a.B, a.ldb, a.b_stride = p.wqa.data_ptr(), d, cfg.d_mem * d
-            a.C, a.ldc, a.c_stride, a.c_dtype = self.qm.data_ptr(), cfg.d_mem, T * cfg.d_mem, F32
-            a.epilogue = EPI_STORE
-            self._tables(a, slots, lrel, gid)
-        args = self._gemm(("q", tuple(slots), tuple(layers)), fill_q)
-        _lib.check(lib.armt_gemm(args, stream), "retrieve q-proj")
         srel = [l - self.layer_base for l in state_layers]
-        mem = self._members(slots, state_layers)
-        _lib.check(lib.armt_dpfp_den(mem, self.qm.data_ptr(), T * cfg.d_mem, state.z.data_ptr(),
-                                     self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
-                                     self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
+        if self.bf16 and FUSED_DPFP and cfg.d_mem in (16, 32, 64) and 1 <= cfg.dpfp_nu <= 3:
+            # q-proj with the DPFP feature map + phi.z in its epilogue: phi (bf16) and den
+            # straight from the accumulator, no q round trip (armt/memory.py:137-147)
+            def fill_qd(a):
+                a.M, a.N, a.K, a.ab_dtype = T, cfg.d_mem, d, p.ab
+                a.A, a.lda, a.a_stride = src.data_ptr(), d, T * d
+                a.B, a.ldb, a.b_stride = p.wqa.data_ptr(), d, cfg.d_mem * d
+                a.C, a.ldc, a.c_stride, a.c_dtype = self.phi.data_ptr(), p.d_phi_pad, T * p.d_phi_pad, BF16
+                a.epilogue = _lib.EPI_DPFP
+                a.den, a.den_stride = self.den.data_ptr(), T
+                a.z, a.nu = state.z.data_ptr(), cfg.dpfp_nu
+                self._tables(a, slots, lrel, gid)
+                for g in range(G):
+                    a.e_index[g] = int(srel[g])
+            args = self._gemm(("qd", tuple(slots), tuple(layers), tuple(state_layers), state.z.data_ptr()), fill_qd)
+            _lib.check(lib.armt_gemm(args, stream), "retrieve q-proj + DPFP")
+        else:
+            def fill_q(a):
+                a.M, a.N, a.K, a.ab_dtype = T, cfg.d_mem, d, p.ab
+                a.A, a.lda, a.a_stride = src.data_ptr(), d, T * d
+                a.B, a.ldb, a.b_stride = p.wqa.data_ptr(), d, cfg.d_mem * d
+                a.C, a.ldc, a.c_stride, a.c_dtype = self.qm.data_ptr(), cfg.d_mem, T * cfg.d_mem, F32
+                a.epilogue = EPI_STORE
+                self._tables(a, slots, lrel, gid)
+            args = self._gemm(("q", tuple(slots), tuple(layers)), fill_q)
+            _lib.check(lib.armt_gemm(args, stream), "retrieve q-proj")
+            mem = self._members(slots, state_layers)
+            _lib.check(lib.armt_dpfp_den(mem, self.qm.data_ptr(), T * cfg.d_mem, state.z.data_ptr(),
+                                         self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
+                                         self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
         bmat = state.memop if self.bf16 else state.A
         ld_b = 3 * p.d_phi_pad if self.bf16 else p.d_phi
         nb_rows = state.memop.shape[1] if self.bf16 else d

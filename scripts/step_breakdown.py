@@ -24,7 +24,7 @@ from paper_2506_05229_b200 import ModelConfig  # noqa: E402
 from paper_2506_05229_b200.engine import prepare_weights  # noqa: E402
 from paper_2506_05229_b200.executors import Session  # noqa: E402
 
-GEMM_NAMES = {0: "store", 1: "residual", 2: "retrieve", 3: "swiglu", 4: "rope", 5: "lse"}
+GEMM_NAMES = {0: "store", 1: "residual", 2: "retrieve", 3: "swiglu", 4: "rope", 5: "lse", 6: "qproj_dpfp"}
 
 
 class Proxy:

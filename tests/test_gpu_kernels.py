@@ -362,3 +362,31 @@ def test_tc_gemm_cta_pair_and_multicast_match_single_cta(epi, monkeypatch):
         assert torch.isfinite(p_).all()
         assert rel(p_, s_) < 1e-6, (epi, rel(p_, s_))
         assert torch.equal(m_, s_), (epi, rel(m_, s_))   # same MMA per tile: bitwise
+
+
+@pytest.mark.parametrize("d_mem,nu", [(64, 3), (16, 3), (32, 2), (64, 1)])
+def test_tc_gemm_dpfp_epilogue(d_mem, nu):
+    """q-projection with the DPFP feature map and phi.z fused into the epilogue
+    (armt/memory.py:34-45,137-147) against torch on the same bf16 operands."""
+    torch.manual_seed(11)
+    G, M, K = 3, 300, 256
+    dphi = 2 * nu * d_mem
+    ld = (dphi + 7) // 8 * 8
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = (torch.randn(5, d_mem, K, device=DEV) * 0.1).bfloat16()
+    z = torch.randn(7, dphi, device=DEV)
+    phi = torch.zeros(G, M, ld, device=DEV, dtype=torch.bfloat16)
+    den = torch.zeros(G, M, device=DEV)
+    layers, zrows = [4, 0, 2], [6, 1, 3]
+    args = gemm_args(G, M, d_mem, K, A, B, phi, BF16, BF16, None, layers, None, epilogue=_lib.EPI_DPFP,
+                     ldc=ld, c_stride=M * ld, den=den.data_ptr(), den_stride=M, z=z.data_ptr(), nu=nu)
+    for g in range(G):
+        args.e_index[g] = zrows[g]
+    _lib.check(LIB.armt_gemm(args, stream()), "gemm dpfp")
+    for g in range(G):
+        q = A[g].float() @ B[layers[g]].float().T
+        r = torch.cat([q.clamp_min(0), (-q).clamp_min(0)], -1)
+        want = torch.cat([r * torch.roll(r, -j, -1) for j in range(1, nu + 1)], -1)
+        assert rel(phi[g, :, :dphi].float(), want) < 5e-3
+        assert torch.count_nonzero(phi[g, :, dphi:]) == 0
+        assert rel(den[g], want @ z[zrows[g]]) < 1e-4
