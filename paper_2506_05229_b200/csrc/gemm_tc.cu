@@ -1076,7 +1076,8 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   }
   // one forked stream per calling stream (callers on different streams stay independent)
   struct Fork { cudaStream_t caller, side; cudaEvent_t fork_ev, join_ev; };
-  static Fork forks[8];
+  constexpr int MAX_FORKS = 32;
+  static Fork forks[MAX_FORKS];
   static int n_forks = 0;
   static std::mutex fork_mu;
   Fork* fk = nullptr;
@@ -1084,8 +1085,12 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(fork_mu);
     for (int i = 0; i < n_forks; ++i)
       if (forks[i].caller == s) fk = &forks[i];
+    if (fk == nullptr && n_forks == MAX_FORKS) {
+      // more calling streams than fork slots: run the remainder after the pair tiles
+      int rc = gemm_rows(a, bn, true, 0, m_pair, s);
+      return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
+    }
     if (fk == nullptr) {
-      ARMT_REQUIRE(n_forks < 8, ARMT_ERR_UNSUPPORTED, "gemm: too many calling streams for the remainder fork");
       fk = &forks[n_forks++];
       fk->caller = s;
       cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking);

@@ -221,7 +221,9 @@ class DeviceBackend:
             fn()
         elif self.mode == "capture":
             g = torch.cuda.CUDAGraph()
-            side = torch.cuda.Stream()
+            if getattr(self, "_cap_stream", None) is None:
+                self._cap_stream = torch.cuda.Stream()   # one capture stream for every step graph
+            side = self._cap_stream
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g, stream=side):

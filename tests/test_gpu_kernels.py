@@ -390,3 +390,33 @@ def test_tc_gemm_dpfp_epilogue(d_mem, nu):
         assert rel(phi[g, :, :dphi].float(), want) < 5e-3
         assert torch.count_nonzero(phi[g, :, dphi:]) == 0
         assert rel(den[g], want @ z[zrows[g]]) < 1e-4
+
+
+def test_tc_gemm_concurrent_remainder_from_many_streams(monkeypatch):
+    """The QKV+RoPE GEMM forks its single-CTA remainder onto a per-caller side
+    stream; callers on more streams than fork slots (e.g. one capture stream per
+    per-step graph) must still get correct results (sequential fallback)."""
+    torch.manual_seed(12)
+    monkeypatch.setenv("ARMT_GEMM_BN", "256")
+    monkeypatch.delenv("ARMT_GEMM_PAIR", raising=False)
+    G, M, K, dh, H = 2, 1152, 1024, 64, 8
+    N = 3 * H * dh
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = (torch.randn(G, N, K, device=DEV) * 0.05).bfloat16()
+    inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+    ang = np.arange(M)[:, None] * inv[None]
+    cos_t = torch.tensor(np.cos(ang).T.copy(), dtype=torch.float32, device=DEV)
+    sin_t = torch.tensor(np.sin(ang).T.copy(), dtype=torch.float32, device=DEV)
+    outs = []
+    for _ in range(40):
+        st = torch.cuda.Stream()
+        C = torch.zeros(G, M, N, device=DEV, dtype=torch.bfloat16)
+        args = gemm_args(G, M, N, K, A, B, C, BF16, BF16, epilogue=_lib.EPI_ROPE, rope_cos=cos_t.data_ptr(),
+                         rope_sin=sin_t.data_ptr(), head_dim=dh, rope_cols=2 * H * dh)
+        st.wait_stream(torch.cuda.current_stream())
+        _lib.check(LIB.armt_gemm(args, st.cuda_stream), "gemm")
+        torch.cuda.current_stream().wait_stream(st)
+        outs.append(C)
+    torch.cuda.synchronize()
+    for C in outs[1:]:
+        assert torch.equal(C, outs[0])
