@@ -219,6 +219,8 @@ def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = Non
 LM_FREE_SMS = int(__import__("os").environ.get("ARMT_LM_FREE_SMS", "16"))
 LM_OVERLAP = __import__("os").environ.get("ARMT_LM_OVERLAP", "0") == "1"
 DUAL = __import__("os").environ.get("ARMT_DUAL", "0") == "1"  # opt-in: +0.3% at C2, see DESIGN §4
+if DUAL:   # concurrent streams need the GEMMs' dynamic tile scheduling (read once by the library)
+    __import__("os").environ.setdefault("ARMT_GEMM_DYN", "1")
 
 
 # =========================================================================
