@@ -53,7 +53,6 @@ struct Params {
   const float* rope_cos; const float* rope_sin; int head_dim; int rope_cols; int rope_ld;
   int swiglu_block;
   int max_ctas;
-  int pf, pf_a;  // L2 prefetch distance in k-blocks for B (and A) tiles; 0 = off
   int row0;    // first row of every member this launch covers (rows [row0, M))
   int* tile_ctr;  // dynamic tile scheduling: {next tile, CTAs done} for this launch (nullptr = static)
   int cst;     // bf16 outputs stored through the smem transpose (coalesced 64 B row segments)
@@ -331,11 +330,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
             tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
             tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, b_row, b_idx);
-          }
-          if (p.pf > 0 && kb + p.pf < p.k_blocks) {
-            // warm L2 with the operand tiles p.pf k-blocks ahead (weights miss to HBM)
-            tma_prefetch_3d(&tmB, (kb + p.pf) * BK, b_row, b_idx);
-            if (p.pf_a) tma_prefetch_3d(&tmA, (kb + p.pf) * BK, a_row, a_slot);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1005,12 +999,6 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     p.cst = (a.c_dtype == ARMT_BF16 || a.epilogue == ARMT_EPI_SWIGLU || a.epilogue == ARMT_EPI_ROPE) &&
             a.ldc % 8 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 && a.c_stride % 8 == 0 &&
             !(ce && ce[0] == '0') ? 1 : 0;
-  }
-  {
-    const char* f = getenv("ARMT_GEMM_PF");
-    p.pf = f ? atoi(f) : 0;
-    const char* fa = getenv("ARMT_GEMM_PF_A");
-    p.pf_a = fa ? atoi(fa) : 0;
   }
   {
     static const bool prof = getenv("ARMT_GEMM_PROF") != nullptr;

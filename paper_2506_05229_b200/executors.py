@@ -214,10 +214,6 @@ def diagonal_plan(n_segments: int, n_layers: int, shuffle_seed: int | None = Non
     return Plan("diagonal", S, L, n_slots, steps)
 
 
-# SMs left to the main stream while an LM head runs beside it (the fold's
-# latency-bound kernels, the next step's small launches)
-LM_FREE_SMS = int(__import__("os").environ.get("ARMT_LM_FREE_SMS", "16"))
-LM_OVERLAP = __import__("os").environ.get("ARMT_LM_OVERLAP", "0") == "1"
 DUAL = __import__("os").environ.get("ARMT_DUAL", "0") == "1"  # opt-in: +0.3% at C2, see DESIGN §4
 if DUAL:   # concurrent streams need the GEMMs' dynamic tile scheduling (read once by the library)
     __import__("os").environ.setdefault("ARMT_GEMM_DYN", "1")
@@ -275,11 +271,6 @@ class Runner:
         self.graph = None
         self.graph_state = None
         self.step_events = None
-        # LM head on a side stream (bf16 engine): it leaves SMs to the memory update
-        from . import _lib
-        self.lm_overlap = prepared.dtype_name == "bf16" and LM_OVERLAP
-        self.lm_ctas = max(1, int(_lib.load().armt_num_sms()) - LM_FREE_SMS)
-        self.side = torch.cuda.Stream(device=dev) if self.lm_overlap else None
 
     def _launch_dual(self, state: MemoryState, stream: int) -> None:
         """Two-stream wavefront. Stream 0 runs each step's members with layer < L/2
@@ -330,53 +321,29 @@ class Runner:
         cur.wait_event(end)
 
     def _launch_all(self, state: MemoryState, stream: int, events=None) -> None:
+        """Issue every step on one stream (``events``: per-step timing pairs)."""
         if self.dual and events is None:
             return self._launch_dual(state, stream)
-        """Issue every step. The LM head of an exiting segment runs on a side
-        stream with ``lm_ctas`` CTAs, overlapping the memory update of its
-        step and the following step(s) on the SMs it leaves free; the main
-        stream waits for it only before that segment's slot is re-embedded."""
-        eng = self.engine
+        eng = self._full_engine() if self.dual else self.engine
         seg = self.cfg.segment_size
-        cur = torch.cuda.ExternalStream(stream, device=self.p.device)
-        overlap = self.lm_overlap and events is None
-        if self.dual:   # timed (per-step events) replays run one stream over all members
-            eng = self._full_engine()
-        pending: dict[int, torch.cuda.Event] = {}   # slot -> LM head done
         for i, st in enumerate(self.plan.steps):
             if events is not None:
                 events[i][0].record()
             for s, slot in st.enters:
-                if slot in pending:
-                    cur.wait_event(pending.pop(slot))
                 eng.embed(self.ids[s * seg:(s + 1) * seg], slot, stream)
             if st.nodes:
                 eng.retrieve(st.slots, st.layers, state, stream, st.state_layers)
                 eng.forward(st.slots, st.layers, stream)
-            lm_stream, ctas = stream, 0
-            if st.exits and overlap:
-                ev = torch.cuda.Event()
-                ev.record(cur)
-                self.side.wait_event(ev)
-                lm_stream, ctas = self.side.cuda_stream, self.lm_ctas
             for k, (s, slot) in enumerate(st.exits):
                 row = (st.exit_rows[k] if st.exit_rows is not None else s) * seg
                 if self.scoring_tokens is not None:
-                    eng.unembed_lse(slot, self.ids, row, self.scoring_tokens, self.lse_part, self.lse_tgt,
-                                    lm_stream, ctas)
+                    eng.unembed_lse(slot, self.ids, row, self.scoring_tokens, self.lse_part, self.lse_tgt, stream)
                 else:
-                    eng.unembed(slot, self.logits, row, lm_stream, ctas)
-            if st.exits and overlap:
-                done = torch.cuda.Event()
-                done.record(self.side)
-                for s, slot in st.exits:
-                    pending[slot] = done
+                    eng.unembed(slot, self.logits, row, stream)
             if st.nodes:
                 eng.update(st.slots, st.layers, state, stream, st.state_layers)
             if events is not None:
                 events[i][1].record()
-        for ev in pending.values():
-            cur.wait_event(ev)
 
     def _full_engine(self):
         """A one-stream engine over the same slots (timed per-step replays)."""

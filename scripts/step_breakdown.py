@@ -63,7 +63,6 @@ def main():
     prep = prepare_weights(w, "bf16")
     del w
     sess = Session(prep, n, schedule=args.schedule, graph=False)
-    sess.runner.lm_overlap = False   # serialise: per-op events on one stream
     tokens = torch.as_tensor(np.random.default_rng([0, n]).integers(0, cfg.vocab_size, n)).cuda()
     sess.forward(tokens)
     torch.cuda.synchronize()
