@@ -224,3 +224,25 @@ def test_minibatch_copies_equal_sequential_bitwise(c1, dtype):
         L = cfg.n_layers
         assert torch.equal(st.A[b * L:(b + 1) * L], ref_state.A)
     assert trace.steps_executed == 4 * cfg.n_layers
+
+
+def test_full_width_c2_layers_match_oracle():
+    """C2 layer shapes at full width (d 2048, 32 heads of 64, d_ff 8192, segment
+    1024 + 128 memory tokens, d_mem 64) through the real kernel paths (CTA-pair
+    / multicast GEMMs, concurrent remainder, fused DPFP, ping-pong attention,
+    tensor-core fold), 2 layers x 3 segments, against the f32 oracle. The vocab
+    is cut to 4096 to keep the CPU oracle to seconds; tolerances as in the
+    small configs (bf16 2e-2, f32 mode 1e-4)."""
+    cfg = ModelConfig(n_layers=2, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024, num_mem_tokens=128,
+                      d_mem=64, vocab_size=4096, eps_assoc=100.0, seed=0)
+    w = conditioned_weights(cfg)
+    tokens = cli_tokens(cfg, 3 * cfg.segment_size - 7, seed=4)
+    want, ostate, _ = O.Oracle(w, cfg, np.float32).run_diagonal(tokens)
+    for dtype in ("bf16", "f32"):
+        st = MemoryState.fresh(cfg)
+        got, _ = run_diagonal(prepare_weights(w, dtype), cfg, tokens, dtype=dtype, state=st)
+        tol = TOL[dtype]
+        assert np.isfinite(got).all()
+        assert relative_error(got, want) < tol, (dtype, relative_error(got, want))
+        assert relative_error(st.A.cpu().numpy(), ostate.A) < tol, dtype
+        assert relative_error(st.z.cpu().numpy(), ostate.z) < tol, dtype
