@@ -180,9 +180,11 @@ def make_weights(cfg, init: str = "reference"):
     return GroupedWeights(config=cfg, **arrays)
 
 
-def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: int = 16):
+def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: int = 16,
+                    n_layers: int | None = None):
     """Oracle (numpy/BLAS f32, all host threads) on full-width cells + one LM head,
-    extrapolated over the schedule: S*L cells + S heads."""
+    extrapolated over the schedule: S*L cells + S heads (``n_layers``: the real L
+    when ``w`` holds only a sample of the layers; every cell costs the same)."""
     import armt_oracle as O
     try:
         from threadpoolctl import threadpool_info
@@ -202,23 +204,32 @@ def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: 
     t1 = time.perf_counter()
     orc.unembed(x)
     t_lm = time.perf_counter() - t1
-    total = n_segments * cfg.n_layers * t_cell + n_segments * t_lm
+    total = n_segments * (n_layers or cfg.n_layers) * t_cell + n_segments * t_lm
     return {"t_cell": t_cell, "t_lm": t_lm, "cells": cells, "total_s": total, "threads": threads,
             "sample_s": cells * t_cell + t_lm}
 
 
 # ---------------------------------------------------------------------------- reference arm
 def reference_arm(args, rank, world):
+    """The reference's CPU path on this host: the oracle port (NumPy/BLAS f32, all
+    threads) timed on full-width cells of the requested config + one LM head and
+    extrapolated over the schedule; weights for a 2-layer sample (per-cell cost is
+    layer-independent). Rank 0 only."""
     if rank != 0:
         return 0
+    from dataclasses import replace as _replace
     from paper_2506_05229_b200 import ModelConfig
-    cfg = ModelConfig(**C2, eps_assoc=EPS_ASSOC, seed=0)
-    n = N_TOKENS if args.segments is None else args.segments * cfg.segment_size
-    S = n // cfg.segment_size
-    w = make_weights(cfg)
+    model, n_cfg, desc = CONFIGS[args.config]
+    cfg = ModelConfig(**model, eps_assoc=EPS_ASSOC, seed=0)
+    n = args.tokens or n_cfg
+    if args.segments is not None:
+        n = args.segments * cfg.segment_size
+    S = -(-n // cfg.segment_size)
+    sample = _replace(cfg, n_layers=min(2, cfg.n_layers))
+    w = make_weights(sample)
     rates, totals = [], []
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_rate(w, cfg, S, budget_s=4.0, max_cells=4)
+        r = cpu_oracle_rate(w, sample, S, budget_s=4.0, max_cells=4, n_layers=cfg.n_layers)
         if i >= args.warmup:
             totals.append(r["total_s"])
             rates.append(n / r["total_s"])
@@ -227,10 +238,10 @@ def reference_arm(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(totals),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded reference init, cli token convention)",
-            "config": {"workload": "C2: LLaMA-3.2-1B-shaped ARMT, seg 1024, 128 mem tokens, 131072 tokens",
+            "config": {"workload": f"{desc}, {n} tokens",
                        "schedule": "oracle cells (schedule-invariant per-cell cost)"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-                             "sample": f"per step: {r['cells']} full-width C2 cells (retrieve+block+fold) + 1 "
+                             "sample": f"per step: {r['cells']} full-width cells (retrieve+block+fold) + 1 "
                                        f"segment LM head in numpy/BLAS f32, extrapolated to {S}x{cfg.n_layers} "
                                        f"cells + {S} heads"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
