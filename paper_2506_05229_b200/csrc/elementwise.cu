@@ -21,6 +21,14 @@ std::atomic<long long>& launch_counter() {
   static std::atomic<long long> c{0};
   return c;
 }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ARMT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int num_sms() {
   static int n = 0;
   static std::once_flag once;

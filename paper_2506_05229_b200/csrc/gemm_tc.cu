@@ -247,6 +247,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if constexpr (CLUSTER) cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, tensor maps): overlap it with the previous kernel's tail
+  pdl_launch_dependents();
+  pdl_wait();
 
   const int tiles_mn = p.tiles_m * p.tiles_n;
   const bool dyn = !CLUSTER && p.tile_ctr != nullptr;
@@ -825,18 +828,32 @@ static int launch(const Maps& m, const Params& p, cudaStream_t s) {
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, p);
     ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 cluster gemm launch: %s", cudaGetErrorString(e));
   } else {
     const int grid = p.num_tiles < cap ? p.num_tiles : cap;
-    kern<<<grid, NUM_THREADS, smem, s>>>(m.a, m.b, m.a2, m.b2, p);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, p);
+    ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   }
   ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
   return ARMT_OK;
