@@ -122,6 +122,10 @@ def run_stage(plan: StagePlan, backend, comm) -> None:
             comm.broadcast(buf, world - 1)
         backend.head(s, buf)
 
+    # hand-offs are asynchronous: the next step's compute does not wait for the
+    # NVLink transfer; a slot is only rewritten by a later receive (same NCCL
+    # stream, ordered after the send) or, on rank 0, by an embed (waits below)
+    sends: dict[int, object] = {}
     for st in plan.steps:
         if st.recv is not None:
             s, slot = st.recv
@@ -132,15 +136,21 @@ def run_stage(plan: StagePlan, backend, comm) -> None:
             pending = None
         if st.enter is not None:
             s, slot = st.enter
+            if slot in sends:
+                sends.pop(slot).wait()
             backend.embed(s, slot)
         if st.nodes:
             backend.step(st.slots, st.layers)
         if st.send is not None:
             s, slot = st.send
-            comm.send(backend.slot_tensor(slot), r + 1)
+            if slot in sends:
+                sends.pop(slot).wait()
+            sends[slot] = comm.isend(backend.slot_tensor(slot), r + 1)
         pending = st.head
     if pending is not None:
         head(pending)
+    for work in sends.values():
+        work.wait()
 
 
 class TorchP2P:
@@ -165,6 +175,13 @@ class TorchP2P:
     def send(self, t, dst):
         self._op(self.dist.send, t, dst, False)
 
+    def isend(self, t, dst):
+        """Asynchronous send; ``.wait()`` on the result before ``t`` is rewritten."""
+        if self.staged and t.is_cuda:
+            h = t.detach().to("cpu")
+            return _Staged(self.dist.isend(h, dst), h)
+        return self.dist.isend(t, dst)
+
     def recv(self, t, src):
         self._op(self.dist.recv, t, src, True)
 
@@ -182,6 +199,17 @@ class TorchP2P:
 
     def all_reduce(self, t):
         self._op(lambda x, _: self.dist.all_reduce(x), t, None, True)
+
+
+class _Staged:
+    """A gloo send handle that keeps its host staging copy alive until waited on."""
+
+    def __init__(self, work, buf):
+        self.work, self.buf = work, buf
+
+    def wait(self):
+        self.work.wait()
+        self.buf = None
 
 
 def torch_empty_like_cpu(x):
