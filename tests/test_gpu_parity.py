@@ -246,3 +246,21 @@ def test_full_width_c2_layers_match_oracle():
         assert relative_error(got, want) < tol, (dtype, relative_error(got, want))
         assert relative_error(st.A.cpu().numpy(), ostate.A) < tol, dtype
         assert relative_error(st.z.cpu().numpy(), ostate.z) < tol, dtype
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_odd_shapes_match_oracle(dtype):
+    """Shapes off every fast path's grid: d 384 (6 heads of 64), d_ff 1000
+    (zero-padded to 1024), segment 200 + 24 memory tokens (T 224: partial m- and
+    attention tiles), d_mem 32 with DPFP order 2, vocab 777, ragged tail."""
+    cfg = ModelConfig(n_layers=3, d_model=384, n_heads=6, d_ff=1000, segment_size=200, num_mem_tokens=24,
+                      d_mem=32, dpfp_nu=2, vocab_size=777, eps_assoc=10.0, seed=3)
+    w = conditioned_weights(cfg)
+    tokens = cli_tokens(cfg, 4 * cfg.segment_size - 37, seed=8)
+    want, ostate, _ = O.Oracle(w, cfg, np.float64).run_diagonal(tokens)
+    st = MemoryState.fresh(cfg)
+    got, _ = run_diagonal(prepare_weights(w, dtype), cfg, tokens, dtype=dtype, state=st)
+    assert relative_error(got, want) < TOL[dtype], relative_error(got, want)
+    assert relative_error(st.A.cpu().numpy(), ostate.A) < TOL[dtype]
+    seq, _ = run_sequential(prepare_weights(w, dtype), cfg, tokens, dtype=dtype)
+    assert np.array_equal(seq, got)
