@@ -18,6 +18,7 @@
 // (~2^-16 relative), accumulated in fp32 TMEM. The f32 parity mode keeps the
 // SIMT fold (memory.cu).
 
+#include <algorithm>
 #include "common.cuh"
 
 namespace armt {
@@ -155,12 +156,13 @@ __global__ void __launch_bounds__(256) fold_phi_kernel(const __grid_constant__ A
 // (armt/memory.py:101-106,116-119 with z_i expanded over earlier tokens);
 // then coef_i, L_ij = coef_i K_ij (j < i), and z_M = z_0 + sum_i gamma_i phi_i.
 constexpr int QMAX = 8;  // M <= 256
+template <int QM>   // register slots per lane for the token chain: ceil(M / 32) <= QM
 __global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__ ArmtMembers mem, float* __restrict__ z,
                                                          __nv_bfloat16* __restrict__ memop, float eps, Geom q, Ws w) {
   extern __shared__ float sm[];
   const int Mp = q.Mp, M = q.M;
   float* sK = sm;                  // [Mp][Mp], K_ij (K is symmetric up to rounding; rows read by lanes)
-  float* szq = sK + Mp * Mp;       // [Mp]
+  float* szq = sK + (Mp * Mp > 4 * q.dphi ? Mp * Mp : 4 * q.dphi);  // (sK region doubles as z partials)
   float* sgam = szq + Mp;          // [Mp]
   float* snrm = sgam + Mp;         // [Mp]
   const int g = blockIdx.x, layer = mem.layer[g];
@@ -183,9 +185,9 @@ __global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__
   __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    float e[QMAX];
+    float e[QM];
 #pragma unroll
-    for (int r = 0; r < QMAX; ++r) {
+    for (int r = 0; r < QM; ++r) {
       const int t = lane + 32 * r;
       e[r] = t < M ? cg[t] : 0.f;
     }
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__
       const int qi = i0 >> 5, l0 = i0 & 31;
       float mine = 0.f;
 #pragma unroll
-      for (int r = 0; r < QMAX; ++r)
+      for (int r = 0; r < QM; ++r)
         if (r == qi) mine = e[r];
       float zq[4], gam[4];
 #pragma unroll
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(512) fold_chain_kernel(const __grid_constant__
         sgam[i0 + lane] = lane == 0 ? gam[0] : lane == 1 ? gam[1] : lane == 2 ? gam[2] : gam[3];
       }
 #pragma unroll
-      for (int r = 0; r < QMAX; ++r) {
+      for (int r = 0; r < QM; ++r) {
         if (r < rmax) {
           const int t = lane + 32 * r;
           if (t >= i0 + 4 && t < M) {
@@ -396,9 +398,14 @@ extern "C" int armt_mem_fold_tc(const ArmtMembers* mem, const float* kvb, long l
     int rc = gemm_tc(a, s);
     if (rc) return rc;
   }
-  const size_t chain_smem = sizeof(float) * ((size_t)q.Mp * q.Mp + 3 * (size_t)q.Mp);
-  cudaFuncSetAttribute(fold_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem);
-  fold_chain_kernel<<<mem->G, 512, chain_smem, s>>>(*mem, z, mo, eps, q, w);
+  const size_t chain_smem = sizeof(float) * ((size_t)std::max(q.Mp * q.Mp, 4 * dphi) + 3 * (size_t)q.Mp);
+  if (n_mem <= 128) {
+    cudaFuncSetAttribute(fold_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem);
+    fold_chain_kernel<4><<<mem->G, 512, chain_smem, s>>>(*mem, z, mo, eps, q, w);
+  } else {
+    cudaFuncSetAttribute(fold_chain_kernel<QMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem);
+    fold_chain_kernel<QMAX><<<mem->G, 512, chain_smem, s>>>(*mem, z, mo, eps, q, w);
+  }
   ARMT_CHECK_LAUNCH("fold_chain");
 
   const size_t solve_smem = sizeof(float) * ((size_t)q.Mp * q.Mp + (size_t)q.Mp * (SOLVE_COLS + 1));
