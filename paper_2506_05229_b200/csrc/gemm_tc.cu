@@ -1062,10 +1062,14 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   // -1.5%, gate/up +7% slower); ARMT_GEMM_PAIR=conc runs that remainder CONCURRENTLY on a
   // forked stream with ARMT_GEMM_REM_CTAS SMs (default 20) while the pair tiles use the rest.
   // Default policy (in-situ step breakdown, same box): whole-pair shapes -> pairs (LM head
-  // -11%); the QKV+RoPE GEMM -> concurrent remainder (-6%); gate/up and down stay single-CTA
-  // (pairs measured +2..4% slower there).
+  // -11%); the QKV+RoPE GEMM and the K=8192 down-projection -> concurrent remainder (-6%,
+  // -9%); gate/up stays a multicast cluster (pairs measured slower there).
   const bool split = pe && strcmp(pe, "split") == 0;
-  const bool conc = (pe && strcmp(pe, "conc") == 0) || (!pe && a.epilogue == ARMT_EPI_ROPE);
+  // the long-K residual GEMM (down-projection) also runs pair tiles + concurrent remainder:
+  // -9% on the op in situ, -1.4% per forward (ARMT_GEMM_CONC_DOWN=0 disables)
+  static const bool conc_down = !(getenv("ARMT_GEMM_CONC_DOWN") && getenv("ARMT_GEMM_CONC_DOWN")[0] == '0');
+  const bool conc = (pe && strcmp(pe, "conc") == 0) ||
+                    (!pe && (a.epilogue == ARMT_EPI_ROPE || (conc_down && a.epilogue == ARMT_EPI_RESIDUAL && a.K >= 4096)));
   const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) &&
                     a.K >= (heavy_epi ? 4096 : 1024) && !(pe && pe[0] == '0');
   if (!pair) {
