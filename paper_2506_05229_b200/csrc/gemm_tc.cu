@@ -984,7 +984,7 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     // dynamic tile scheduling: a fresh {next, done} counter pair per launch from a ring in
     // device memory (each launch's last CTA re-zeroes its pair, so graph replays reuse it)
     static int* ring = nullptr;
-    static unsigned long long next = 0;
+    static std::atomic<unsigned long long> next{0};
     constexpr unsigned long long RING = 1ull << 18;
     // opt-in (ARMT_GEMM_DYN=1, set by the dual-stream runner): one-stream runs are 0.4%
     // faster with the static schedule, concurrent streams need the dynamic one
@@ -996,7 +996,7 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
         ARMT_REQUIRE(cudaMalloc(&ring, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring alloc");
         ARMT_REQUIRE(cudaMemset(ring, 0, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring init");
       }
-      p.tile_ctr = ring + 2 * (next++ % RING);
+      p.tile_ctr = ring + 2 * (next.fetch_add(1) % RING);
     }
   }
   if (p.max_ctas == 0) {   // experiments: ARMT_GEMM_MAXCTAS caps every launch
