@@ -983,21 +983,25 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   if (!pair && !mc) {
     // dynamic tile scheduling: a fresh {next, done} counter pair per launch from a ring in
     // device memory (each launch's last CTA re-zeroes its pair, so graph replays reuse it)
-    static int* ring = nullptr;
+    static std::atomic<int*> ring{nullptr};
+    static std::mutex ring_mu;
     static std::atomic<unsigned long long> next{0};
     constexpr unsigned long long RING = 1ull << 18;
     // opt-in (ARMT_GEMM_DYN=1, set by the dual-stream runner): one-stream runs are 0.4%
     // faster with the static schedule, concurrent streams need the dynamic one
     static const bool dyn_on = getenv("ARMT_GEMM_DYN") && getenv("ARMT_GEMM_DYN")[0] == '1';
-    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
-    if (ring == nullptr) cudaStreamIsCapturing(s, &cap_st);   // (no allocation inside a graph capture)
-    if (dyn_on && (ring != nullptr || cap_st == cudaStreamCaptureStatusNone)) {
-      if (ring == nullptr) {
-        ARMT_REQUIRE(cudaMalloc(&ring, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring alloc");
-        ARMT_REQUIRE(cudaMemset(ring, 0, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring init");
+    if (dyn_on && ring.load() == nullptr) {
+      cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(s, &cap_st);   // (no allocation inside a graph capture: static schedule)
+      std::lock_guard<std::mutex> lk(ring_mu);
+      if (cap_st == cudaStreamCaptureStatusNone && ring.load() == nullptr) {
+        int* r = nullptr;
+        ARMT_REQUIRE(cudaMalloc(&r, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring alloc");
+        ARMT_REQUIRE(cudaMemset(r, 0, RING * 2 * sizeof(int)) == cudaSuccess, ARMT_ERR_CUDA, "tile ring init");
+        ring.store(r);
       }
-      p.tile_ctr = ring + 2 * (next.fetch_add(1) % RING);
     }
+    if (dyn_on && ring.load() != nullptr) p.tile_ctr = ring.load() + 2 * (next.fetch_add(1) % RING);
   }
   if (p.max_ctas == 0) {   // experiments: ARMT_GEMM_MAXCTAS caps every launch
     static const char* mc = getenv("ARMT_GEMM_MAXCTAS");
