@@ -1072,10 +1072,13 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   // the long-K residual GEMM (down-projection) also runs pair tiles + concurrent remainder:
   // -9% on the op in situ, -1.4% per forward (ARMT_GEMM_CONC_DOWN=0 disables)
   static const bool conc_down = !(getenv("ARMT_GEMM_CONC_DOWN") && getenv("ARMT_GEMM_CONC_DOWN")[0] == '0');
+  // ... and so does the O-projection residual GEMM (-0.5% per forward; ARMT_GEMM_CONC_O=0 disables)
+  static const bool conc_o = !(getenv("ARMT_GEMM_CONC_O") && getenv("ARMT_GEMM_CONC_O")[0] == '0');
   const bool conc = (pe && strcmp(pe, "conc") == 0) ||
-                    (!pe && (a.epilogue == ARMT_EPI_ROPE || (conc_down && a.epilogue == ARMT_EPI_RESIDUAL && a.K >= 4096)));
+                    (!pe && (a.epilogue == ARMT_EPI_ROPE || (conc_down && a.epilogue == ARMT_EPI_RESIDUAL && a.K >= 4096) ||
+                             (conc_o && a.epilogue == ARMT_EPI_RESIDUAL)));
   const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) &&
-                    a.K >= (heavy_epi ? 4096 : 1024) && !(pe && pe[0] == '0');
+                    a.K >= (heavy_epi && !conc_o ? 4096 : 1024) && !(pe && pe[0] == '0');
   if (!pair) {
     // multicast clusters (ARMT_GEMM_MC=0 disables): 256-wide tiles, an even number of
     // n-blocks (pair slots), mainloop-heavy shapes
