@@ -881,7 +881,11 @@ static int pick_bn(const ArmtGemmArgs& a) {
     const double fill = (double)tiles / (double)(waves * sms);      // wave quantisation
     const double useful = (double)a.N / (double)(tn * bn);          // N padding
     const double size = bn == 256 ? 1.0 : bn == 128 ? 0.93 : 0.8;   // per-tile efficiency
-    const double score = fill * useful * size;
+    // a single wave leaves every CTA's epilogue exposed (nothing to overlap it with):
+    // small grouped GEMMs (memory-token k/v/beta, fold) prefer two tiles per CTA
+    static const bool w1pen = !(getenv("ARMT_GEMM_W1PEN") && getenv("ARMT_GEMM_W1PEN")[0] == '0');
+    const double one_wave = (w1pen && waves == 1 && tiles > sms / 2) ? 0.8 : 1.0;
+    const double score = fill * useful * size * one_wave;
     if (score > best_score + 1e-9) { best_score = score; best = bn; }
   }
   return best;
