@@ -6,7 +6,7 @@
 Writes profiles/<tag>_launches.md (per-kernel share of device time from the
 cold-cache, serialised launch list) and profiles/<tag>_kernels.json + .md
 (key metrics of each full capture: duration, DRAM bytes, tensor-pipe %, L2 %,
-DRAM %, issue %, registers). bench.py reads the gate/up GEMM's DRAM bytes
+derived DRAM GB/s and % of measured HBM, issue %, registers). bench.py reads the gate/up GEMM's DRAM bytes
 from profiles/*_kernels.json as its roofline `traffic`.
 """
 
@@ -27,7 +27,8 @@ METRICS = {
     "dram_write_bytes": "dram__bytes_write.sum",
     "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-    "dram_throughput_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+                            "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
     "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -75,8 +76,9 @@ def full_metrics(rep):
         if len(v) != len(h):
             continue
         res = {"kernel": short(v[h.index("Kernel Name")]) if "Kernel Name" in h else ""}
-        for key, m in METRICS.items():
-            if m in h:
+        for key, names in METRICS.items():
+            m = next((n for n in ((names,) if isinstance(names, str) else names) if n in h), None)
+            if m is not None:
                 try:
                     res[key] = float(v[h.index(m)].replace(",", ""))
                 except ValueError:
@@ -85,12 +87,35 @@ def full_metrics(rep):
     return res_all
 
 
+def write_kernels_md(res, out_dir, tag, note):
+    """DRAM GB/s is derived (bytes / duration) and set against the measured
+    copy bandwidth in MEASURED_PEAKS.json, so the column never depends on
+    which throughput-percentage name this ncu version exports."""
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = json.load(open(peaks_path)).get("hbm_gbs") if os.path.exists(peaks_path) else None
+    lines = [f"# {tag}: ncu --set full captures (one launch each)", "", note, "",
+             f"DRAM GB/s = (dram__bytes_read.sum + dram__bytes_write.sum) / gpu__time_duration.sum; "
+             f"% HBM is against the measured copy bandwidth ({hbm} GB/s, MEASURED_PEAKS.json).", "",
+             "| capture | kernel | us | DRAM MB (r+w) | DRAM GB/s | % HBM | tensor % | L2 % | issue % | regs |",
+             "|---|---|---:|---:|---:|---:|---:|---:|---:|---:|"]
+    for label, m in res.items():
+        dram = (m.get("dram_read_bytes", 0) + m.get("dram_write_bytes", 0)) / 1e6
+        ns = m.get("duration_ns", 0)
+        gbs = dram * 1e6 / ns if ns else 0.0
+        pct = f"{gbs / hbm * 100:.1f}" if hbm else "-"
+        lines.append(f"| {label} | `{m.get('kernel', '')}` | {ns / 1e3:.1f} | {dram:.1f} | {gbs:.0f} | {pct} | "
+                     f"{m.get('tensor_pipe_pct', 0):.1f} | {m.get('l2_throughput_pct', 0):.1f} | "
+                     f"{m.get('issue_active_pct', 0):.1f} | {m.get('registers', 0):.0f} |")
+    open(os.path.join(out_dir, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
     ap.add_argument("--full", action="append", default=[])
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--note", default="")
+    ap.add_argument("--from-json", help="rewrite <tag>_kernels.md from an existing <tag>_kernels.json")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles"))
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
@@ -110,16 +135,10 @@ def main():
             for k, m in enumerate(full_metrics(rep)):
                 res[label if k == 0 else f"{label}.{k}"] = m
         json.dump(res, open(os.path.join(args.out, f"{args.tag}_kernels.json"), "w"), indent=1)
-        lines = [f"# {args.tag}: ncu --set full captures (one launch each)", "", args.note, "",
-                 "| capture | kernel | us | DRAM MB (r+w) | tensor % | L2 % | DRAM % | issue % | regs |",
-                 "|---|---|---:|---:|---:|---:|---:|---:|---:|"]
-        for label, m in res.items():
-            dram = (m.get("dram_read_bytes", 0) + m.get("dram_write_bytes", 0)) / 1e6
-            lines.append(f"| {label} | `{m.get('kernel', '')}` | {m.get('duration_ns', 0) / 1e3:.1f} | {dram:.1f} | "
-                         f"{m.get('tensor_pipe_pct', 0):.1f} | {m.get('l2_throughput_pct', 0):.1f} | "
-                         f"{m.get('dram_throughput_pct', 0):.1f} | {m.get('issue_active_pct', 0):.1f} | "
-                         f"{m.get('registers', 0):.0f} |")
-        open(os.path.join(args.out, f"{args.tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+        write_kernels_md(res, args.out, args.tag, args.note)
+    if args.from_json:
+        res = json.load(open(args.from_json))
+        write_kernels_md(res, args.out, args.tag, args.note)
 
 
 if __name__ == "__main__":
