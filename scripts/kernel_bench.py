@@ -96,6 +96,36 @@ def gemm_specs(G, rows=None):
             "lm": (1, 1024, V, d, _lib.EPI_STORE, BF16)}
 
 
+def cublas_op(G, Mr, N, K, epi, c_dtype):
+    """The same grouped GEMM through cuBLAS (torch.bmm, one weight per member),
+    GEMM alone and with the epilogue as separate torch ops - the unfused
+    library baseline the fused kernel replaces."""
+    A = torch.randn(G, Mr, K, device="cuda").bfloat16()
+    B = (torch.randn(G, N, K, device="cuda") * 0.02).bfloat16()
+    Bt = B.transpose(1, 2)
+    C = torch.empty(G, Mr, N, device="cuda", dtype=torch.bfloat16)
+    gemm_only = lambda: torch.bmm(A, Bt, out=C)
+    ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
+    R = torch.zeros(G, Mr, ncol, device="cuda")
+    R16 = torch.empty(G, Mr, ncol, device="cuda", dtype=torch.bfloat16)
+    den = torch.ones(G, Mr, 1, device="cuda")
+    cs = torch.rand(Mr, ncol // 2, device="cuda")
+
+    def full():
+        torch.bmm(A, Bt, out=C)
+        if epi == _lib.EPI_SWIGLU:
+            g, u = C.chunk(2, dim=-1)
+            torch.mul(torch.nn.functional.silu(g), u, out=R16)
+        elif epi in (_lib.EPI_RESIDUAL, _lib.EPI_RETRIEVE):
+            R.add_(C.float() / den if epi == _lib.EPI_RETRIEVE else C.float())
+            R16.copy_(R)
+            R.view(G, Mr, -1, 64).pow(2).sum(-1)
+        elif epi == _lib.EPI_ROPE:
+            x = C.float().view(G, Mr, ncol // 2, 2)
+            torch.stack((x[..., 0] * cs - x[..., 1] * cs, x[..., 0] * cs + x[..., 1] * cs), -1).bfloat16()
+    return gemm_only, full, [A, B, C, R, R16, den, cs]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--G", type=int, default=16)
@@ -106,6 +136,7 @@ def main():
     ap.add_argument("--rows", type=int, default=None, help="rows per member (default T)")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--prof", action="store_true", help="GEMM wait-cycle counters (ARMT_GEMM_PROF)")
+    ap.add_argument("--cublas", action="store_true", help="also time each GEMM op through cuBLAS (torch.bmm)")
     args = ap.parse_args()
     if args.flags:
         for rep in range(args.repeat):
@@ -139,6 +170,12 @@ def main():
                 rec.update(mma_wait_full=buf[0] / tot, mma_wait_acc=buf[1] / tot, prod_wait_empty=buf[3] / tot,
                            tiles=buf[4], epi_wait_full_per_tile=buf[5] / max(buf[4], 1) / 8,
                            mma_cycles_per_cta=tot / min(148, buf[4]))
+            if args.cublas:
+                del keep
+                g_only, full, keep = cublas_op(*spec)
+                us_g, us_f = timeit(g_only, args.iters), timeit(full, args.iters)
+                rec.update(cublas_gemm_us=us_g, cublas_gemm_tflops=flops / us_g / 1e6, cublas_unfused_us=us_f,
+                           speedup_vs_cublas_gemm=us_g / us, speedup_vs_cublas_unfused=us_f / us)
             print(json.dumps(rec), flush=True)
         elif op == "attn":
             qkv = torch.randn(G, T, 3 * d, device="cuda").bfloat16()
@@ -148,8 +185,16 @@ def main():
                                                        BF16, T, H, dh, 1 / math.sqrt(dh), s), "attn")
             us = timeit(fn, args.iters)
             flops = G * 4 * d * T * (T + 1) / 2
-            print(json.dumps({"op": "attn", "G": G, "us": us, "tflops": flops / us / 1e6,
-                              "frac_sustained": flops / us / 1e6 / pk["bf16_tflops_sustained"]}), flush=True)
+            rec = {"op": "attn", "G": G, "us": us, "tflops": flops / us / 1e6,
+                   "frac_sustained": flops / us / 1e6 / pk["bf16_tflops_sustained"]}
+            if args.cublas:
+                # library baseline: torch SDPA (flash / cuDNN backends) on the same causal
+                # problem, q/k/v already split into (G, H, T, dh) - the layout work is not timed
+                q, k, v = (t.view(G, T, H, dh).transpose(1, 2).contiguous() for t in qkv.split(d, dim=-1))
+                sdpa = lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+                us_s = timeit(sdpa, args.iters)
+                rec.update(sdpa_us=us_s, sdpa_tflops=flops / us_s / 1e6, speedup_vs_sdpa=us_s / us)
+            print(json.dumps(rec), flush=True)
         elif op == "foldtc":
             dphi, P = 6 * dm, 6 * dm
             A = torch.randn(L, d, dphi, device="cuda") * 0.01
