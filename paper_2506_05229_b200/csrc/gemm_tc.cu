@@ -272,7 +272,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   // consumer side of the queue: entry k (MMA reads every k, epilogue group eg every k = eg mod 2)
   auto tq_pop = [&](int k, bool epi_warp) -> int {
     const int qs = k % QD;
-    mbar_wait(&tq_full[qs], (uint32_t)((k / QD) & 1));
+    mbar_wait_sleep(&tq_full[qs], (uint32_t)((k / QD) & 1));
     const int t = tq_ids[qs];
     if (!epi_warp || lane == 0) mbar_arrive(&tq_empty[qs]);
     return t;
@@ -415,11 +415,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int c_slot = p.c_slot[g];
       if (p.prof && lane == 0) {
         const long long t0 = clock64();
-        mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait_sleep(&tfull[acc], acc_phase);
         atomicAdd(&g_gemm_prof[5], (unsigned long long)(clock64() - t0));
       }
       __syncwarp();
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
