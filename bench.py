@@ -386,10 +386,35 @@ def device_arm(args, rank, world):
     e2e_value = n / (e2e_total / args.steps / 1e3)
     mean_nll = float(host_nll.mean())
 
+    # north-star ratio in the same run: the sequential segment schedule (armt/executors.py:123-150),
+    # same kernels (G = 1 lane), same whole-run CUDA-graph policy, same K/W, fresh memory per replay
+    seq_value = None
+    d_ff_pad = sess.p.d_ff_pad
+    if args.compare_sequential and world == 1 and not args.force_sharded and args.schedule == "diagonal":
+        del sess
+        torch.cuda.empty_cache()
+        seq = Session(prep, n, schedule="sequential", scoring=scoring_value)
+        seq._load_ids(torch.as_tensor(tokens).to(dev))
+        seq.warm()
+        for _ in range(args.warmup):
+            seq.forward()
+        torch.cuda.synchronize()
+        seq_ms = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            seq.forward()
+            e1.record()
+            torch.cuda.synchronize()
+            seq_ms.append(e0.elapsed_time(e1))
+        seq_value = n / (statistics.mean(seq_ms) / 1e3)
+        del seq
+        torch.cuda.empty_cache()
+
     peaks, peak_kind = load_peaks()
     traffic = (load_traffic("gemm_gu" if probe_g == 16 else f"gemm_gu_g{probe_g}")
                if (args.config == "c2" and full_g == 16) else None)
-    d_ff_pad = sess.p.d_ff_pad
     gu_bytes = 2.0 * (probe_g * cfg.tokens_per_segment * cfg.d_model + probe_g * 2 * d_ff_pad * cfg.d_model
                       + probe_g * cfg.tokens_per_segment * d_ff_pad)
     # dominant kernel: the grouped tcgen05 GEMM; probed launch = full-width gate/up (SwiGLU epilogue)
@@ -438,6 +463,9 @@ def device_arm(args, rank, world):
                        if not sharded else "ShardedSession(scoring=True).nll: pinned ids in, per-token NLL out "
                                           "(vocab-parallel fused NLL, all-gathered row partials)",
                 "mean_nll": mean_nll},
+        "sequential_value": seq_value,
+        "diag_over_seq": (value / seq_value) if seq_value else None,
+        "north_star_target": "diagonal >= 1.8x sequential on 1xB200 at C2" if seq_value else None,
         "gpu_launches": int(launches_per_forward * args.steps),
         "clocks": clocks.summary(),
     }
@@ -460,6 +488,8 @@ def main():
     ap.add_argument("--eps", type=float, default=None, help="eps_assoc override (fixture conditioning)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the layer-sharded session even at world size 1 (plumbing check)")
+    ap.add_argument("--no-sequential", dest="compare_sequential", action="store_false",
+                    help="skip timing the sequential schedule (north-star diag/seq ratio)")
     ap.add_argument("--scoring", action="store_true",
                     help="time the fused-NLL forward (no logits) for the value too (implied for c4)")
     args = ap.parse_args()

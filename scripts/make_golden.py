@@ -79,9 +79,63 @@ def run_both(w, cfg, tokens, dtype):
     return seq, st_s, nodes
 
 
+def _trace_cfg(L):
+    return ModelConfig(n_layers=L, d_model=8, n_heads=2, d_ff=8, segment_size=2,
+                       num_mem_tokens=1, d_mem=1, vocab_size=7, seed=1)
+
+
+def make_traces():
+    """Reference node lists of run_diagonal (plain and under shuffle_seed, the
+    reference's member-order audit hook, armt/executors.py:192-195) and of
+    run_sequential, for several (S, L) grids."""
+    grids = [(4, 3), (3, 2), (1, 5), (5, 1), (7, 4)]
+    tr = {}
+    for S, L in grids:
+        cfg = _trace_cfg(L)
+        toks = np.arange(S * 2) % 7
+        _, trace = run_diagonal(init_weights(cfg), cfg, toks)
+        flat = [[n.segment, n.layer] for ev in trace.events for n in ev.nodes]
+        tr[f"nodes_{S}x{L}"] = np.array(flat, np.int64)
+        tr[f"counts_{S}x{L}"] = np.array([len(ev.nodes) for ev in trace.events], np.int64)
+    for S, L, seed in [(4, 3, 7), (7, 4, 123), (9, 6, 2024), (16, 16, 5)]:
+        cfg = _trace_cfg(L)
+        toks = np.arange(S * 2) % 7
+        _, trace = run_diagonal(init_weights(cfg), cfg, toks, shuffle_seed=seed)
+        flat = [[n.segment, n.layer] for ev in trace.events for n in ev.nodes]
+        tr[f"shuf_nodes_{S}x{L}_seed{seed}"] = np.array(flat, np.int64)
+        tr[f"shuf_counts_{S}x{L}_seed{seed}"] = np.array([len(ev.nodes) for ev in trace.events], np.int64)
+    for S, L in [(3, 4)]:
+        cfg = _trace_cfg(L)
+        _, trace = run_sequential(init_weights(cfg), cfg, np.arange(S * 2) % 7)
+        tr[f"seq_nodes_{S}x{L}"] = np.array([[n.segment, n.layer] for ev in trace.events for n in ev.nodes],
+                                            np.int64)
+    np.savez_compressed(os.path.join(OUT, "traces.npz"), **tr)
+
+
+def make_containers():
+    """Weight containers written by the reference's own save_weights
+    (armt/weights.py:145-171): the reference's test config (tests/test_container.py:12-16)
+    in f64 and f32 payloads, and a C1-shaped f32 container that the GPU loader test runs."""
+    from armt import save_weights
+    cfg = ModelConfig(n_layers=2, d_model=8, n_heads=2, d_ff=12, segment_size=3,
+                      num_mem_tokens=2, d_mem=3, vocab_size=17, seed=5)
+    w = init_weights(cfg)
+    save_weights(w, os.path.join(OUT, "ref_tiny_f64.armt"))
+    w32 = replace(w, **{k: v.astype(np.float32) for k, v in w.named_arrays().items()})
+    save_weights(w32, os.path.join(OUT, "ref_tiny_f32.armt"))
+    cfg = ModelConfig(**C1, eps_assoc=1.0, seed=0)
+    wc = conditioned(cfg)
+    wc = replace(wc, **{k: v.astype(np.float32) for k, v in wc.named_arrays().items()})
+    save_weights(wc, os.path.join(OUT, "ref_c1_cond_f32.armt"))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("reference armt", armt.__version__)
+    if len(sys.argv) > 1:   # e.g. `make_golden.py traces containers`: regenerate only those
+        for name in sys.argv[1:]:
+            globals()["make_" + name]()
+        return
 
     # -- small_ref: the reference's own fixture ----------------------------
     cfg = ModelConfig(n_layers=3, d_model=16, n_heads=2, d_ff=32, segment_size=6,
@@ -144,18 +198,8 @@ def main():
                     f"forward_{dt}": y, f"A1_{dt}": st.A, f"z1_{dt}": st.z})
     np.savez_compressed(os.path.join(OUT, "ops_c1.npz"), **out)
 
-    # -- traces -------------------------------------------------------------
-    grids = [(4, 3), (3, 2), (1, 5), (5, 1), (7, 4)]
-    tr = {}
-    for S, L in grids:
-        cfg = ModelConfig(n_layers=L, d_model=8, n_heads=2, d_ff=8, segment_size=2,
-                          num_mem_tokens=1, d_mem=1, vocab_size=7, seed=1)
-        toks = np.arange(S * 2) % 7
-        _, trace = run_diagonal(init_weights(cfg), cfg, toks)
-        flat = [[n.segment, n.layer] for ev in trace.events for n in ev.nodes]
-        tr[f"nodes_{S}x{L}"] = np.array(flat, np.int64)
-        tr[f"counts_{S}x{L}"] = np.array([len(ev.nodes) for ev in trace.events], np.int64)
-    np.savez_compressed(os.path.join(OUT, "traces.npz"), **tr)
+    make_traces()
+    make_containers()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

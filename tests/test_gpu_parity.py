@@ -264,3 +264,68 @@ def test_odd_shapes_match_oracle(dtype):
     assert relative_error(st.A.cpu().numpy(), ostate.A) < TOL[dtype]
     seq, _ = run_sequential(prepare_weights(w, dtype), cfg, tokens, dtype=dtype)
     assert np.array_equal(seq, got)
+
+
+@pytest.fixture(scope="module")
+def c2_full_depth():
+    """The headline model at FULL depth and width: 16 layers, d 2048, 32 heads of
+    64, d_ff 8192, segment 1024 + 128 memory tokens, d_mem 64, the bench's
+    eps_assoc 100 conditioning; the vocab is cut to 4096 so the f32 CPU oracle
+    finishes in about a minute (the LM head does not feed the recurrence).
+    3 segments with a ragged tail: 48 cells, 18 wavefront steps, up to 3 members."""
+    cfg = ModelConfig(n_layers=16, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024, num_mem_tokens=128,
+                      d_mem=64, vocab_size=4096, eps_assoc=100.0, seed=0)
+    w = conditioned_weights(cfg)
+    tokens = cli_tokens(cfg, 3 * cfg.segment_size - 13, seed=2)
+    want, ostate, _ = O.Oracle(w, cfg, np.float32).run_diagonal(tokens)
+    return cfg, w, tokens, want, ostate
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_full_depth_c2_matches_oracle(c2_full_depth, dtype):
+    """North-star tolerances at the headline config's depth: f32 mode 1e-4 and
+    bf16 2e-2 relative (logits, A, z) against the f32 oracle, per segment too."""
+    cfg, w, tokens, want, ostate = c2_full_depth
+    st = MemoryState.fresh(cfg)
+    got, trace = run_diagonal(prepare_weights(w, dtype), cfg, tokens, dtype=dtype, state=st)
+    tol = TOL[dtype]
+    assert np.isfinite(got).all()
+    seg = cfg.segment_size
+    per_seg = [relative_error(got[s * seg:(s + 1) * seg], want[s * seg:(s + 1) * seg]) for s in range(3)]
+    assert max(per_seg) < tol, (dtype, per_seg)
+    assert relative_error(got, want) < tol
+    assert relative_error(st.A.cpu().numpy(), ostate.A) < tol, dtype
+    assert relative_error(st.z.cpu().numpy(), ostate.z) < tol, dtype
+    assert st.updates.tolist() == [3] * 16
+    assert trace.steps_executed == 3 + 16 - 1
+
+
+def test_full_depth_c2_memory_is_live(c2_full_depth):
+    """The parity above is only meaningful if the memory changes the outputs:
+    with W_k = 0 (nothing stored, every read guarded) the logits of segments
+    1-2 must move by well over the f32 tolerance (segment 0 reads an empty
+    memory either way, so it must not move at all)."""
+    cfg, w, tokens, _, _ = c2_full_depth
+    live, _ = run_diagonal(prepare_weights(w, "f32"), cfg, tokens, dtype="f32")
+    inert_w = replace(w, w_k_mem=np.zeros_like(w.w_k_mem))
+    inert, _ = run_diagonal(prepare_weights(inert_w, "f32"), cfg, tokens, dtype="f32")
+    seg = cfg.segment_size
+    assert np.array_equal(live[:seg], inert[:seg])
+    moved = relative_error(live[seg:], inert[seg:])
+    assert moved > 1e-2, moved
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_reference_written_container_drives_the_device(dtype):
+    """a weight file written by the reference's own
+    save_weights (tests/golden/ref_c1_cond_f32.armt) loads here and drives the
+    device path to the reference's C1 logits and memory state."""
+    import os
+    from conftest import GOLDEN
+    w = P.load_weights(os.path.join(GOLDEN, "ref_c1_cond_f32.armt"))
+    cfg = w.config
+    g = golden("c1_cond")
+    state = MemoryState.fresh(cfg)
+    logits, _ = run_diagonal(w, cfg, g["tokens"], dtype=dtype, state=state)
+    assert relative_error(logits, g["logits_f64"]) < TOL[dtype]
+    assert relative_error(state.A.cpu().numpy(), g["A_f64"]) < TOL[dtype]
