@@ -308,7 +308,7 @@ def device_arm(args, rank, world):
     sess.warm_eager()
     sharded = world > 1 or args.force_sharded
     for e in engines:
-        e.probe = None if sharded else make_probe(e)   # (per-step graphs of the sharded path: no probe)
+        e.probe = make_probe(e)   # (sharded path: event-record nodes inside the per-step graphs)
     sess.capture()
     for e in engines:
         e.probe = None

@@ -109,6 +109,10 @@ int armt_gemm(const ArmtGemmArgs* args, void* stream);
 int armt_embed(const long long* ids, const void* emb, const void* mem_emb, int w_dtype,
                float* x, void* x_bf, int seg, int n_mem, int d, int vocab, void* stream);
 
+/* Ids outside [0, vocab) seen by armt_embed since the last reset (their rows
+ * are written as zeros, never gathered). Synchronous; -1 on a CUDA error. */
+long long armt_embed_bad_ids(int reset);
+
 /* Replaces rms_norm_stacked (armt/tensor_ops.py:267-281):
  * out[g] = x[slot[g]] / sqrt(mean(x^2) + eps) * gain[layer[g]]. */
 int armt_rmsnorm(const ArmtMembers* mem, const float* x, long long x_stride,

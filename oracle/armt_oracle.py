@@ -152,13 +152,14 @@ def block(x: np.ndarray, lw: LayerWeights, n_heads: int, eps_norm: float,
 
 
 def fold(A: np.ndarray, z: np.ndarray, m: np.ndarray, lw: LayerWeights, nu: int,
-         eps: float) -> None:
+         eps: float, log: list | None = None) -> None:
     """Delta-rule write of M memory-token outputs, in token order, in place
     (armt/memory.py:155-180 projections, armt/memory.py:94-125 fold).
 
     For token i: zq = z.phi_i, nrm = phi_i.phi_i;
     vbar = |zq| <= eps ? 0 : (A phi_i)/zq; gamma = nrm <= eps ? 0 : 1 - zq/nrm;
     A += beta_i (v_i - vbar) phi_i^T; z += gamma phi_i.
+    ``log`` (test diagnostics) receives (zq, nrm) for every token.
     """
     k = m @ lw.w_k_mem.T
     v = m @ lw.w_v_mem.T
@@ -168,6 +169,8 @@ def fold(A: np.ndarray, z: np.ndarray, m: np.ndarray, lw: LayerWeights, nu: int,
         p = phi[i]
         zq = float(z @ p)
         nrm = float(p @ p)
+        if log is not None:
+            log.append((zq, nrm))
         vbar = np.zeros(A.shape[0], A.dtype) if abs(zq) <= eps else (A @ p) / zq
         gamma = 0.0 if nrm <= eps else 1.0 - zq / nrm
         A += np.outer(beta[i] * (v[i] - vbar), p)
@@ -218,6 +221,7 @@ class Oracle:
         self.mem_embedding = np.asarray(weights.mem_embedding, self.dtype)
         self.unembedding = np.asarray(weights.unembedding, self.dtype)
         self.cos, self.sin = rope_tables(self.T, self.dh, self.dtype)
+        self.fold_log = None   # set to a list to record (layer, [(zq, nrm) per token]) per fold
 
     def embed(self, ids):
         """armt/layers.py:306-318."""
@@ -229,7 +233,10 @@ class Oracle:
         lw = self.layers[l]
         x = retrieve(state.A[l], state.z[l], x, lw.w_q_assoc, cfg.dpfp_nu, self.eps)
         y = block(x, lw, cfg.n_heads, cfg.eps_norm, self.cos, self.sin)
-        fold(state.A[l], state.z[l], y[cfg.segment_size:], lw, cfg.dpfp_nu, self.eps)
+        rows = [] if self.fold_log is not None else None
+        fold(state.A[l], state.z[l], y[cfg.segment_size:], lw, cfg.dpfp_nu, self.eps, rows)
+        if rows is not None:
+            self.fold_log.append((l, rows))
         state.updates[l] += 1
         return y
 

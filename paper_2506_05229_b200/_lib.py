@@ -26,7 +26,7 @@ EXPORTS = ("armt_gemm", "armt_embed", "armt_rmsnorm", "armt_dpfp_den", "armt_att
            "armt_rope", "armt_swiglu", "armt_mem_fold", "armt_fold_workspace_bytes", "armt_cast",
            "armt_logits_nll", "armt_last_error", "armt_version", "armt_num_sms",
            "armt_kernel_count", "armt_abi_sizeof", "armt_mem_fold_tc", "armt_fold_tc_workspace_bytes",
-           "armt_memop_rows", "armt_lse_finalize", "armt_lse_reduce", "armt_gemm_prof")
+           "armt_memop_rows", "armt_lse_finalize", "armt_lse_reduce", "armt_gemm_prof", "armt_embed_bad_ids")
 
 _I = ctypes.c_int
 _LL = ctypes.c_longlong
@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
     sig = {
         "armt_gemm": (_I, [ctypes.POINTER(ArmtGemmArgs), _P]),
         "armt_embed": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _P]),
+        "armt_embed_bad_ids": (_LL, [_I]),
         "armt_rmsnorm": (_I, [ctypes.POINTER(ArmtMembers), _P, _LL, _P, _P, _I, _LL, _I, _I, _F, _P]),
         "armt_dpfp_den": (_I, [ctypes.POINTER(ArmtMembers), _P, _LL, _P, _P, _I, _LL, _LL, _P, _LL,
                                _I, _I, _I, _P]),

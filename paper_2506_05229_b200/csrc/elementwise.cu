@@ -44,16 +44,24 @@ int num_sms() {
 // ------------------------------------------------------------------ embed
 // armt/layers.py:306-318: rows [0, seg) from the embedding table, rows
 // [seg, seg+M) from mem_embedding (memory rows last).
+// Ids outside [0, vocab) never index the table: their row is written as zeros
+// and counted in g_bad_ids (armt_embed_bad_ids), so a bad id cannot fault or
+// read foreign memory inside a captured graph; the Python layer validates ids
+// before launch and raises InputError like the reference (armt/layers.py:311-315).
+__device__ unsigned int g_bad_ids = 0;
+
 __global__ void embed_kernel(const long long* __restrict__ ids, const void* emb, const void* mem_emb,
                              int w_dtype, float* __restrict__ x, __nv_bfloat16* __restrict__ x_bf,
-                             int seg, int n_mem, int d) {
+                             int seg, int n_mem, int d, int vocab) {
   const int row = blockIdx.x;
   const void* src;
   long long src_row;
   if (row < seg) { src = emb; src_row = ids[row]; }
   else { src = mem_emb; src_row = row - seg; }
+  const bool bad = row < seg && (src_row < 0 || src_row >= vocab);
+  if (bad && threadIdx.x == 0) atomicAdd(&g_bad_ids, 1u);
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    const float v = load_as_f32(src, w_dtype, src_row * d + c);
+    const float v = bad ? 0.f : load_as_f32(src, w_dtype, src_row * d + c);
     x[(long long)row * d + c] = v;
     if (x_bf) x_bf[(long long)row * d + c] = __float2bfloat16_rn(v);
   }
@@ -257,9 +265,20 @@ int armt_embed(const long long* ids, const void* emb, const void* mem_emb, int w
   ARMT_REQUIRE(ids && emb && mem_emb && x, ARMT_ERR_INPUT, "embed: null pointer");
   ARMT_REQUIRE(seg >= 1 && n_mem >= 0 && d >= 1 && vocab >= 1, ARMT_ERR_DIM, "embed: bad sizes");
   embed_kernel<<<seg + n_mem, 128, 0, as_stream(stream)>>>(ids, emb, mem_emb, w_dtype, x,
-                                                           reinterpret_cast<__nv_bfloat16*>(x_bf), seg, n_mem, d);
+                                                           reinterpret_cast<__nv_bfloat16*>(x_bf), seg, n_mem, d,
+                                                           vocab);
   ARMT_CHECK_LAUNCH("embed");
   return ARMT_OK;
+}
+
+long long armt_embed_bad_ids(int reset) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, g_bad_ids, sizeof(n)) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned int zero = 0;
+    if (cudaMemcpyToSymbol(g_bad_ids, &zero, sizeof(zero)) != cudaSuccess) return -1;
+  }
+  return (long long)n;
 }
 
 int armt_rmsnorm(const ArmtMembers* mem, const float* x, long long x_stride, const float* gain, void* out,

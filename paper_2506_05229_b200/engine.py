@@ -87,6 +87,7 @@ class PreparedWeights:
     rope_cos_t: torch.Tensor      # (d_head/2, T): fused QKV epilogue (bf16 mode)
     rope_sin_t: torch.Tensor
     layer_base: int = 0
+    vocab_base: int = 0            # first unembedding column held (vocab-parallel head)
 
     @property
     def ab(self) -> int:
@@ -106,11 +107,15 @@ class PreparedWeights:
 
 
 def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=None,
-                    layers: range | None = None) -> PreparedWeights:
+                    layers: range | None = None, vocab: range | None = None,
+                    embedding: bool = True) -> PreparedWeights:
     """Cast, transpose to K-major, pad and upload (one-time setup).
 
     ``layers`` restricts the per-layer tensors to a contiguous block (layer
     sharding); layer indices stay global in the executors and are rebased here.
+    ``vocab`` uploads only that block of unembedding columns (vocab-parallel
+    LM head; ``vocab_base`` records its start) and ``embedding=False`` skips
+    the token embedding (pipeline stages other than the first).
     """
     cfg = weights.config
     resolve_dtype(dtype_name)
@@ -173,20 +178,38 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
         config=cfg, dtype_name=dtype_name, eps_assoc=cfg.effective_eps_assoc(dtype_name),
         device=dev, wdtype=wdt, T=T, d_head=dh, d_phi=d_phi, d_phi_pad=d_phi_pad,
         d_ff_pad=d_ff_pad, swiglu_block=block, n_kvb=n_kvb,
-        embedding=up("embedding", False).to(wdt), mem_embedding=up("mem_embedding", False).to(wdt),
+        embedding=(up("embedding", False).to(wdt) if embedding
+                   else torch.zeros(0, d, dtype=wdt, device=dev)),
+        mem_embedding=up("mem_embedding", False).to(wdt),
         wqkv=wqkv, wo=wo, wgu=wgu, wdown=wdown,
         attn_gain=g_attn.contiguous(), mlp_gain=g_mlp.contiguous(),
         unit_gain=torch.ones_like(g_attn).contiguous(),
         wqa=up("w_q_assoc").to(wdt).contiguous(), wkvb=wkvb.to(wdt),
-        unemb=up("unembedding", False).t().contiguous().to(wdt),
+        unemb=_unemb(weights.unembedding, vocab, dev, wdt),
         rope_cos=torch.as_tensor(np.cos(ang), dtype=torch.float32).to(dev).contiguous(),
         rope_sin=torch.as_tensor(np.sin(ang), dtype=torch.float32).to(dev).contiguous(),
         rope_cos_t=torch.as_tensor(np.cos(ang).T, dtype=torch.float32).to(dev).contiguous(),
         rope_sin_t=torch.as_tensor(np.sin(ang).T, dtype=torch.float32).to(dev).contiguous(),
     )
     prepared.layer_base = lo
+    prepared.vocab_base = 0 if vocab is None else vocab.start
     torch.cuda.synchronize(dev)
     return prepared
+
+
+def _unemb(u, vocab: range | None, dev, wdt) -> torch.Tensor:
+    """(V, d) K-major unembedding (or its [v0, v1) row block), uploaded column
+    block by column block so the host never materialises a second full copy."""
+    V = u.shape[1]
+    v0, v1 = (0, V) if vocab is None else (vocab.start, vocab.stop)
+    out = torch.empty(v1 - v0, u.shape[0], dtype=wdt, device=dev)
+    step = 16384
+    for a in range(v0, v1, step):
+        b = min(v1, a + step)
+        blk = u[:, a:b]
+        t = blk if isinstance(blk, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(blk))
+        out[a - v0:b - v0] = t.to(dev, torch.float32).t().to(wdt)
+    return out
 
 
 # ============================================================================
@@ -312,7 +335,11 @@ class Engine:
         self.fold_ws = torch.zeros(max(nb, 16) // 4 + 1, device=dev)  # zero padding is part of the contract
         # fused RMSNorm (bf16, full step path): per-row sum of squares produced by the
         # residual epilogues, consumed (and re-zeroed) by the next GEMM's epilogue
-        self.fused = self.bf16 and fused_norm
+        # the QKV epilogue applies RoPE for head sizes {8,16,32,64,128}; other (even) head
+        # sizes run QKV with a plain store + the stand-alone RoPE kernel, and then the
+        # RMSNorm cannot ride in that epilogue either (armt/layers.py:169-176 allows any even d_head)
+        self.rope_fused = self.bf16 and p.d_head in (8, 16, 32, 64, 128)
+        self.fused = self.bf16 and fused_norm and self.rope_fused
         self.ssq_np = (d + 63) // 64
         self.ssq_attn = torch.zeros(G, T, self.ssq_np, device=dev)
         self.ssq_mlp = torch.zeros(G, T, self.ssq_np, device=dev)
@@ -349,6 +376,8 @@ class Engine:
         """armt/layers.py:306-318 into activation slot ``slot``."""
         p, cfg = self.p, self.cfg
         T, d = p.T, cfg.d_model
+        if p.embedding.shape[0] != cfg.vocab_size:
+            raise InputError("these prepared weights hold no token embedding (prepare_weights(embedding=False))")
         xb = None if self.xs_bf is None else self.xs_bf[slot].data_ptr()
         _lib.check(self.lib.armt_embed(ids.data_ptr(), p.embedding.data_ptr(), p.mem_embedding.data_ptr(),
                                        p.ab, self.xs[slot].data_ptr(), xb, cfg.segment_size,
@@ -441,7 +470,7 @@ class Engine:
             a.A, a.lda, a.a_stride = a_in.data_ptr(), d, T * d
             a.B, a.ldb, a.b_stride = p.wqkv.data_ptr(), d, 3 * d * d
             a.C, a.ldc, a.c_stride, a.c_dtype = self.qkv.data_ptr(), 3 * d, T * 3 * d, wout
-            if self.bf16:
+            if self.rope_fused:
                 a.epilogue = EPI_ROPE
                 a.rope_cos, a.rope_sin = p.rope_cos_t.data_ptr(), p.rope_sin_t.data_ptr()
                 a.head_dim, a.rope_cols = p.d_head, 2 * d
@@ -452,8 +481,8 @@ class Engine:
                 a.epilogue = EPI_STORE
             self._tables(a, a_idx, lrel, gid)
         _lib.check(lib.armt_gemm(self._gemm(("qkv",) + key, fill_qkv), stream), "qkv")
-        if not self.bf16:
-            _lib.check(lib.armt_rope(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, F32, T, cfg.n_heads, p.d_head,
+        if not self.rope_fused:
+            _lib.check(lib.armt_rope(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, wout, T, cfg.n_heads, p.d_head,
                                      p.rope_cos.data_ptr(), p.rope_sin.data_ptr(), stream), "rope")
         _lib.check(lib.armt_attention(G, self.qkv.data_ptr(), 3 * d, T * 3 * d, self.ctx.data_ptr(), d, T * d,
                                       wout, T, cfg.n_heads, p.d_head, 1.0 / math.sqrt(p.d_head), stream),
@@ -516,12 +545,15 @@ class Engine:
     def update(self, slots, layers, state: MemoryState, stream: int, state_layers=None) -> None:
         """update_stack (armt/memory.py:155-180) from the memory rows of xs[slots]
         (``state_layers``: see ``retrieve``)."""
-        if state_layers is None:
-            state_layers = layers
+        if self.cfg.num_mem_tokens == 0:
+            return
+        self.project_kvb(slots, layers, stream)
+        self.fold(slots, layers, state, stream, state_layers)
+
+    def project_kvb(self, slots, layers, stream: int) -> None:
+        """k, v, beta projections of the memory rows (armt/memory.py:166-171) into ``self.kvb``."""
         p, cfg, lib = self.p, self.cfg, self.lib
         T, d, M = p.T, cfg.d_model, cfg.num_mem_tokens
-        if M == 0:
-            return
         lrel = [l - self.layer_base for l in layers]
         gid = list(range(len(layers)))
         src = self.xs_bf if self.bf16 else self.xs
@@ -535,6 +567,14 @@ class Engine:
             a.epilogue = EPI_STORE
             self._tables(a, slots, lrel, gid)
         _lib.check(lib.armt_gemm(self._gemm(("kvb", tuple(slots), tuple(layers)), fill_kvb), stream), "kvb")
+
+    def fold(self, slots, layers, state: MemoryState, stream: int, state_layers=None) -> None:
+        """The delta-rule fold of update_stack (armt/memory.py:94-125, 175-180) from
+        the k/v/beta projections already in ``self.kvb``."""
+        if state_layers is None:
+            state_layers = layers
+        p, cfg, lib = self.p, self.cfg, self.lib
+        d, M = cfg.d_model, cfg.num_mem_tokens
         mem = self._members(slots, state_layers)
         if self.bf16:
             _lib.check(lib.armt_mem_fold_tc(mem, self.kvb.data_ptr(), p.n_kvb, M * p.n_kvb, p.v_off, p.k_off,
@@ -552,6 +592,10 @@ class Engine:
         self.forward(slots, layers, stream)
         self.update(slots, layers, state, stream, state_layers)
 
+    def _full_vocab(self) -> None:
+        if self.p.unemb.shape[0] != self.cfg.vocab_size:
+            raise InputError("these prepared weights hold one vocab block; use unembed_block")
+
     def unembed_lse(self, slot: int, ids: torch.Tensor, row0: int, n_tokens: int, part: torch.Tensor,
                     tgt: torch.Tensor, stream: int, max_ctas: int = 0) -> None:
         """LM head with the fused next-token NLL epilogue: no logits are written;
@@ -561,6 +605,7 @@ class Engine:
         src = self.xs_bf if self.bf16 else self.xs
         rows = max(0, min(seg, n_tokens - 1 - row0))
         tiles = part.shape[1]
+        self._full_vocab()
 
         def fill(a):
             a.M, a.N, a.K, a.ab_dtype = seg, V, d, p.ab
@@ -582,6 +627,7 @@ class Engine:
         d, V, seg = cfg.d_model, cfg.vocab_size, cfg.segment_size
         src = self.xs_bf if self.bf16 else self.xs
         odt = BF16 if out.dtype == torch.bfloat16 else F32
+        self._full_vocab()
 
         def fill(a):
             a.M, a.N, a.K, a.ab_dtype = seg, V, d, p.ab
@@ -608,7 +654,10 @@ class Engine:
         def fill(a):
             a.M, a.N, a.K, a.ab_dtype = seg, nv, d, p.ab
             a.A, a.lda, a.a_stride = a_ptr, a_ld, seg * a_ld
-            a.B, a.ldb, a.b_stride = p.unemb.data_ptr() + v0 * d * p.unemb.element_size(), d, V * d
+            if not (p.vocab_base <= v0 <= v1 <= p.vocab_base + p.unemb.shape[0]):
+                raise InputError(f"vocab block [{v0}, {v1}) not held by these weights "
+                                 f"(columns {p.vocab_base}..{p.vocab_base + p.unemb.shape[0]})")
+            a.B, a.ldb, a.b_stride = p.unemb.data_ptr() + (v0 - p.vocab_base) * d * p.unemb.element_size(), d, V * d
             if lse is None:
                 odt = BF16 if out.dtype == torch.bfloat16 else F32
                 a.C, a.ldc, a.c_stride, a.c_dtype = out.data_ptr() + row0 * nv * out.element_size(), nv, seg * nv, odt

@@ -83,6 +83,18 @@ def segment_input(tokens, config: ModelConfig) -> tuple[list[np.ndarray], int]:
     return list(ids.reshape(-1, config.segment_size)), n
 
 
+def check_ids(ids: torch.Tensor, vocab: int, what: str = "token ids") -> None:
+    """Device-tensor counterpart of segment_input's range check (one aminmax
+    and a host read): ids outside [0, vocab) raise InputError before launch."""
+    if ids.dtype not in (torch.int64, torch.int32):
+        raise InputError(f"{what} must be an integer tensor, got {ids.dtype}")
+    if ids.numel() == 0:
+        raise InputError(f"{what}: empty")
+    lo, hi = torch.aminmax(ids)
+    if int(lo) < 0 or int(hi) >= vocab:
+        raise InputError(f"{what} must lie in [0, {vocab})")
+
+
 def relative_error(a, b) -> float:
     """||a - b||_F / ||b||_F in f64; both-zero is 0 (armt/executors.py:233-247)."""
     if isinstance(a, torch.Tensor):
@@ -550,6 +562,7 @@ class Session:
         if isinstance(tokens, torch.Tensor):
             if tokens.numel() != self.n:
                 raise InputError(f"session compiled for {self.n} tokens, got {tokens.numel()}")
+            check_ids(tokens, self.cfg.vocab_size)
             ids[:self.n].copy_(tokens.reshape(-1), non_blocking=True)
         else:
             segs, n = segment_input(tokens, self.cfg)
@@ -606,6 +619,11 @@ class Session:
         logits = self.forward(tokens)
         if targets is None:
             targets = self.runner.ids[1:self.n]
+        else:
+            if not isinstance(targets, torch.Tensor) or targets.dtype != torch.int64 or targets.numel() != self.n - 1:
+                raise InputError(f"targets must be an int64 tensor of {self.n - 1} ids")
+            targets = targets.to(self.p.device).reshape(-1).contiguous()
+            check_ids(targets, self.cfg.vocab_size, "target ids")
         odt = _lib.BF16 if logits.dtype == torch.bfloat16 else _lib.F32
         _lib.check(_lib.load().armt_logits_nll(logits.data_ptr(), odt, self.cfg.vocab_size, targets.data_ptr(),
                                                self.nll_rows.data_ptr(), self.n - 1, self.cfg.vocab_size,

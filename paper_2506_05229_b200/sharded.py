@@ -108,49 +108,66 @@ def stage_plan(n_segments: int, n_layers: int, rank: int, world: int) -> StagePl
 
 
 def run_stage(plan: StagePlan, backend, comm) -> None:
-    """Drive one rank through every global step. ``comm`` has send(t, dst),
+    """Drive one rank through every global step. ``comm`` has isend(t, dst),
     recv(t, src) and broadcast(t, src) (torch.distributed: NCCL on GPUs, gloo
     in tests). ``backend`` exposes slot_tensor / after_recv / embed / step /
-    head_buffer / head."""
+    head_buffer / head.
+
+    Per step: receive (from rank-1) -> embed (rank 0) -> this rank's cells ->
+    asynchronous send (to rank+1) -> the deferred vocab-parallel LM head of the
+    segment that left layer L-1 on the previous step (broadcast + head GEMM).
+    So every rank's point-to-point traffic of a step is posted before that
+    step's collective (no cross-rank ordering deadlock), and the head is off
+    the path between a rank's cells and the send the next rank waits for.
+
+    Buffer reuse: a slot with a send in flight is never rewritten (by a
+    receive or an embed) before that send's ``wait()`` — on NCCL this orders
+    the compute stream after the transfer without blocking the host. The
+    last rank's exiting slot is read by the head one step after its exit and
+    rewritten no earlier than two steps after it (``n_slots`` = layers + 1).
+    """
     r, world = plan.rank, plan.world
     pending = None
-
-    def head(h):
-        s, slot = h
-        buf = backend.head_buffer(slot)
-        if world > 1:
-            comm.broadcast(buf, world - 1)
-        backend.head(s, buf)
-
-    # hand-offs are asynchronous: the next step's compute does not wait for the
-    # NVLink transfer; a slot is only rewritten by a later receive (same NCCL
-    # stream, ordered after the send) or, on rank 0, by an embed (waits below)
     sends: dict[int, object] = {}
+
+    def settle(slot):
+        work = sends.pop(slot, None)
+        if work is not None:
+            work.wait()
+
     for st in plan.steps:
         if st.recv is not None:
             s, slot = st.recv
+            settle(slot)
             comm.recv(backend.slot_tensor(slot), r - 1)
             backend.after_recv(slot)
-        if pending is not None:
-            head(pending)
-            pending = None
         if st.enter is not None:
             s, slot = st.enter
-            if slot in sends:
-                sends.pop(slot).wait()
+            settle(slot)
             backend.embed(s, slot)
         if st.nodes:
             backend.step(st.slots, st.layers)
         if st.send is not None:
             s, slot = st.send
-            if slot in sends:
-                sends.pop(slot).wait()
+            settle(slot)
             sends[slot] = comm.isend(backend.slot_tensor(slot), r + 1)
+        if pending is not None:
+            _head(backend, comm, pending, world)
         pending = st.head
     if pending is not None:
-        head(pending)
+        _head(backend, comm, pending, world)
     for work in sends.values():
         work.wait()
+
+
+def _head(backend, comm, h, world) -> None:
+    """Vocab-parallel LM head of one exiting segment: the last rank's token
+    rows are broadcast to every rank, each computes its vocab block."""
+    s, slot = h
+    buf = backend.head_buffer(slot)
+    if world > 1:
+        comm.broadcast(buf, world - 1)
+    backend.head(s, buf)
 
 
 class TorchP2P:
@@ -323,12 +340,13 @@ class ShardedSession:
         seg = cfg.segment_size
         self.plan = stage_plan(S, cfg.n_layers, rank, world)
         blk = self.plan.layers
-        self.p = prepare_weights(weights, "bf16", device, layers=blk)
+        self.vocab = vocab_blocks(cfg.vocab_size, world)[rank]
+        # this rank's layers, its vocab block of the unembedding, the embedding only on stage 0
+        self.p = prepare_weights(weights, "bf16", device, layers=blk, vocab=self.vocab, embedding=blk.start == 0)
         dev = self.p.device
         self.engine = Engine(self.p, self.plan.max_members, self.plan.n_slots)
         self.state = MemoryState.fresh(cfg, dev, n_layers=len(blk))
         self.ids = torch.zeros(S * seg, dtype=torch.int64, device=dev)
-        self.vocab = vocab_blocks(cfg.vocab_size, world)[rank]
         nv = len(self.vocab)
         self.scoring = scoring
         self.logits = None
@@ -358,7 +376,12 @@ class ShardedSession:
 
     def _load_ids(self, tokens):
         import torch
-        self.ids[:self.n].copy_(torch.as_tensor(tokens).reshape(-1).to(self.ids.device), non_blocking=True)
+        from .executors import check_ids
+        t = torch.as_tensor(tokens).reshape(-1).to(self.ids.device)
+        if t.numel() != self.n:
+            raise InputError(f"session compiled for {self.n} tokens, got {t.numel()}")
+        check_ids(t, self.cfg.vocab_size)
+        self.ids[:self.n].copy_(t, non_blocking=True)
         if self.n < self.ids.numel():
             self.ids[self.n:].zero_()
         if self.scoring:

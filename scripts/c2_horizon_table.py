@@ -18,6 +18,8 @@ Modes
   bf16          production path (fused norms, tcgen05 GEMMs, tensor-core fold)
   bf16_fold32   bf16, but the memory update (k/v/beta projection + fold) in fp32
   bf16_mem32    bf16 backbone, memory read AND update in fp32
+  bf16_kvb32    bf16, k/v/beta projection in fp32 from the fp32 stream, tensor-core fold
+  bf16_tcfold32 bf16, bf16 k/v/beta projection, fp32 in-order fold (isolates the fold)
   f32_inert     f32 with W_k = 0: the memory never stores anything (liveness)
   bf16_inert    bf16 with W_k = 0
 
@@ -66,7 +68,7 @@ def run_mode(mode, w_b, w_f, cfg, ids, S, cols, guard=None):
         if need_b else None
     pf = prepare_weights(w_f if not inert else replace(w_f, w_k_mem=np.zeros_like(w_f.w_k_mem)), "f32") \
         if need_f else None
-    fused = base == "bf16" or base == "bf16_fold32"
+    fused = base in ("bf16", "bf16_fold32", "bf16_kvb32", "bf16_tcfold32")
     eb = Engine(pb, G, plan.n_slots, fused_norm=fused) if need_b else None
     ef = Engine(pf, G, plan.n_slots, slots_from=eb) if need_f else None
     e_ret = ef if base in ("f32", "bf16_mem32") else eb
@@ -92,9 +94,19 @@ def run_mode(mode, w_b, w_f, cfg, ids, S, cols, guard=None):
         for s, slot in st.exits:
             e_fwd.unembed(slot, lm, 0, stream)
             out[s * seg:(s + 1) * seg] = lm[:, :cols].float()
-        e_upd.update(st.slots, st.layers, state, stream)
-        if e_upd is ef and need_b and e_ret is eb:
-            state.sync_shadow(pb)   # the bf16 retrieval reads the split operand; refresh it from fp32 A, z
+        if base == "bf16_kvb32":      # fp32 k/v/beta projection (from the fp32 stream), tensor-core fold
+            ef.project_kvb(st.slots, st.layers, stream)
+            eb.kvb[:len(st.layers)].copy_(ef.kvb[:len(st.layers)])
+            eb.fold(st.slots, st.layers, state, stream)
+        elif base == "bf16_tcfold32":  # bf16 projection (from the bf16 stream copy), fp32 in-order fold
+            eb.project_kvb(st.slots, st.layers, stream)
+            ef.kvb[:len(st.layers)].copy_(eb.kvb[:len(st.layers)])
+            ef.fold(st.slots, st.layers, state, stream)
+            state.sync_shadow(pb)
+        else:
+            e_upd.update(st.slots, st.layers, state, stream)
+            if e_upd is ef and need_b and e_ret is eb:
+                state.sync_shadow(pb)   # the bf16 retrieval reads the split operand; refresh it from fp32 A, z
     torch.cuda.synchronize()
     dt = time.time() - t0
     A = state.A.clone()

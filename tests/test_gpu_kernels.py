@@ -258,6 +258,71 @@ def test_fold_matches_oracle(d, M, d_mem, eps):
     assert torch.equal(A[1].cpu(), torch.tensor(A0[1]))  # untouched layer
 
 
+def _fold64(A0, z0, kvb_g, d, d_mem, nu, eps):
+    """In-order delta rule in f64 (armt/memory.py:94-125) on the device fold's inputs."""
+    import armt_oracle as O
+    Ar, zr = A0.astype(np.float64).copy(), z0.astype(np.float64).copy()
+    k = kvb_g[:, d:d + d_mem].astype(np.float64)
+    v = kvb_g[:, :d].astype(np.float64)
+    beta = O.sigmoid(kvb_g[:, d + d_mem].astype(np.float64))
+    phi = O.dpfp(k, nu)
+    for i in range(k.shape[0]):
+        p = phi[i]
+        zq, nrm = zr @ p, p @ p
+        vbar = np.zeros(d) if abs(zq) <= eps else (Ar @ p) / zq
+        gam = 0.0 if nrm <= eps else 1 - zq / nrm
+        Ar += np.outer(beta[i] * (v[i] - vbar), p)
+        zr += gam * p
+    return Ar, zr
+
+
+@pytest.mark.parametrize("d,M,d_mem,nu,eps", [(2048, 128, 64, 3, 100.0), (2048, 128, 64, 3, 1.0),
+                                              (256, 16, 16, 3, 10.0), (384, 24, 32, 2, 10.0),
+                                              (128, 16, 16, 3, 1e-6)])
+def test_tensor_core_fold_matches_in_order_f64(d, M, d_mem, nu, eps):
+    """armt_mem_fold_tc (chunked form: bf16x3 tensor-core GEMMs + blocked
+    triangular solve) against the in-order f64 delta rule on a LIVE state
+    (nonzero A, z): A and z within 1e-5 relative, untouched layers bitwise,
+    and the bf16x3 memory operand it refreshes equal to a fresh split of the
+    new A and z (the retrieval reads it)."""
+    from types import SimpleNamespace
+    from paper_2506_05229_b200.engine import MemoryState
+    rng = np.random.default_rng(11)
+    dphi = 2 * nu * d_mem
+    P = (dphi + 7) // 8 * 8
+    G, L = 3, 4
+    layers = [3, 0, 2]
+    A0 = (rng.standard_normal((L, d, dphi)) * 0.05).astype(np.float32)
+    z0 = (np.abs(rng.standard_normal((L, dphi))) * 3).astype(np.float32)
+    n_kvb = ((d + d_mem + 1 + 15) // 16) * 16
+    kvb = np.zeros((G, M, n_kvb), np.float32)
+    kvb[:, :, :d] = rng.standard_normal((G, M, d))
+    kvb[:, :, d:d + d_mem] = rng.standard_normal((G, M, d_mem))
+    kvb[:, :, d + d_mem] = rng.standard_normal((G, M))
+    st = MemoryState(A=torch.tensor(A0, device=DEV), z=torch.tensor(z0, device=DEV), updates=np.zeros(L, np.int64))
+    prep = SimpleNamespace(dtype_name="bf16", d_phi_pad=P, config=SimpleNamespace(num_mem_tokens=M))
+    st.sync_shadow(prep)
+    kv = torch.tensor(kvb, device=DEV)
+    ws = torch.zeros(LIB.armt_fold_tc_workspace_bytes(G, M, d, dphi) // 4 + 1, device=DEV)
+    mem = _lib.members([0, 1, 2], layers)
+    _lib.check(LIB.armt_mem_fold_tc(mem, kv.data_ptr(), n_kvb, M * n_kvb, 0, d, d + d_mem, st.A.data_ptr(),
+                                    st.z.data_ptr(), st.memop.data_ptr(), d, M, d_mem, nu, eps, ws.data_ptr(),
+                                    stream()), "fold_tc")
+    torch.cuda.synchronize()
+    for g, l in enumerate(layers):
+        Ar, zr = _fold64(A0[l], z0[l], kvb[g], d, d_mem, nu, eps)
+        assert rel(st.A[l].cpu(), torch.tensor(Ar)) < 1e-5, (l, rel(st.A[l].cpu(), torch.tensor(Ar)))
+        assert rel(st.z[l].cpu(), torch.tensor(zr)) < 1e-5
+    assert torch.equal(st.A[1].cpu(), torch.tensor(A0[1]))
+    # the refreshed operand: rows 0..d-1 = [hi | lo | hi] of A, row d = that of z
+    op = st.memop.float()
+    for l in layers:
+        hi, lo = op[l, :d, :dphi], op[l, :d, P:P + dphi]
+        assert rel(hi + lo, st.A[l]) < 2e-5
+        assert torch.equal(op[l, :d, 2 * P:2 * P + dphi], op[l, :d, :dphi])
+        assert rel(op[l, d, :dphi] + op[l, d, P:P + dphi], st.z[l]) < 2e-5
+
+
 def test_rmsnorm_matches_reference():
     torch.manual_seed(8)
     G, T, d, L = 3, 100, 256, 4

@@ -145,3 +145,84 @@ def test_two_rank_gloo_pipeline_equals_unsharded_oracle():
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
     assert np.array_equal(results[0][1], wstate.A[0:1])
     assert np.array_equal(results[1][1], wstate.A[1:2])
+
+
+class _LogComm:
+    """Records the order of communication calls (no data moves)."""
+
+    def __init__(self, log):
+        self.log = log
+
+    def isend(self, t, dst):
+        self.log.append(("isend", dst, id(t)))
+        log, key = self.log, id(t)
+
+        class _W:
+            def wait(self_inner):
+                log.append(("wait", key))
+        return _W()
+
+    def recv(self, t, src):
+        self.log.append(("recv", src, id(t)))
+
+    def broadcast(self, t, src):
+        self.log.append(("broadcast", src))
+
+
+class _LogBackend:
+    def __init__(self, log, n_slots):
+        self.log = log
+        self.slots = [torch.zeros(1) for _ in range(n_slots)]
+
+    def slot_tensor(self, slot):
+        return self.slots[slot]
+
+    def after_recv(self, slot):
+        pass
+
+    def embed(self, s, slot):
+        self.log.append(("embed", id(self.slots[slot])))
+
+    def step(self, slots, layers):
+        self.log.append(("step", tuple(layers)))
+
+    def head_buffer(self, slot):
+        return self.slots[slot] if slot is not None else torch.zeros(1)
+
+    def head(self, s, buf):
+        self.log.append(("head", s))
+
+
+@pytest.mark.parametrize("S,L,P", [(8, 16, 4), (20, 16, 8), (5, 6, 3), (3, 4, 2)])
+def test_stage_ordering_sends_before_collective_and_no_slot_reuse_in_flight(S, L, P):
+    """Every rank posts a step's cells and its send BEFORE the deferred head
+    broadcast of that step (the head is off the path between a rank's cells and
+    the send its successor waits for), and no slot with a send in flight is
+    rewritten (received into or embedded) before that send was waited on."""
+    for r in range(P):
+        plan = stage_plan(S, L, r, P)
+        log = []
+        run_stage(plan, _LogBackend(log, plan.n_slots), _LogComm(log))
+        in_flight = set()
+        for ev in log:
+            if ev[0] == "isend":
+                assert ev[2] not in in_flight
+                in_flight.add(ev[2])
+            elif ev[0] == "wait":
+                in_flight.discard(ev[1])
+            elif ev[0] in ("recv", "embed"):
+                buf = ev[2] if ev[0] == "recv" else ev[1]
+                assert buf not in in_flight, (r, ev)
+        heads = [k for k, ev in enumerate(log) if ev[0] == "head"]
+        assert [log[k][1] for k in heads] == list(range(S))
+        if P > 1:
+            assert sum(1 for ev in log if ev[0] == "broadcast") == S
+        idx_step = [k for k, ev in enumerate(log) if ev[0] == "step"]
+        idx_send = [k for k, ev in enumerate(log) if ev[0] == "isend"]
+        cell_steps = [i for i, st in enumerate(plan.steps) if st.nodes]
+        for s, k in enumerate(heads):
+            i_head = s + L   # segment s leaves layer L-1 at step s+L-1; its head runs after step s+L's work
+            done = {i for i, kk in zip(cell_steps, idx_step) if kk < k}
+            assert done == {i for i in cell_steps if i <= i_head}
+            sends = sum(1 for kk in idx_send if kk < k)
+            assert sends == sum(1 for st in plan.steps[:i_head + 1] if st.send is not None)
