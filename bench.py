@@ -210,43 +210,143 @@ def cpu_oracle_rate(w, cfg, n_segments: int, budget_s: float = 12.0, max_cells: 
 
 
 # ---------------------------------------------------------------------------- reference arm
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")   # pip install --target of /root/reference/pkg (git-ignored)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ReferenceCells:
+    """The UNMODIFIED reference package (baseline/_ref, numba kernels) on this
+    host's cores, through its own public API: one diagonal step of ``G`` members
+    at the model's full width (retrieve_stack -> forward_stack -> update_stack
+    with WorkerPool(cpu_count), armt/executors.py:196-203) on a short segment,
+    plus its own ``gemm`` for ``lm_rows`` LM-head rows at the full vocabulary
+    (armt/layers.py:321-323). Numba's loops cost the same for any values, so the
+    rates measured here extrapolate by FLOPs to full C2 cells and segments."""
+
+    def __init__(self, model: dict, eps: float, seg: int = 32, lm_rows: int = 4, members: int | None = None):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        import armt
+        from armt.layers import forward_stack
+        from armt.memory import retrieve_stack, update_stack
+        self.armt, self.fwd, self.ret, self.upd = armt, forward_stack, retrieve_stack, update_stack
+        self.cores = os.cpu_count() or 1
+        G = members or min(16, self.cores, model["n_layers"])
+        self.cfg = armt.ModelConfig(**dict(model, n_layers=G, segment_size=seg, vocab_size=512),
+                                    eps_assoc=eps, seed=0)
+        w = armt.init_weights(self.cfg)
+        self.p = armt.prepare_weights(w, "f32")
+        del w
+        self.state = armt.MemoryState.fresh(self.cfg, "f32")
+        self.pool = armt.WorkerPool(self.cores)
+        rng = np.random.default_rng(0)
+        self.x = np.stack([armt.embed_segment(self.p, rng.integers(0, 512, seg), i).data for i in range(G)])
+        self.layers = np.arange(G, dtype=np.int64)
+        self.G, self.seg, self.lm_rows = G, seg, lm_rows
+        self.V = model["vocab_size"]
+        self.U = np.random.default_rng(1).standard_normal((model["d_model"], self.V), dtype=np.float32)
+        armt.tensor_ops.warmup_kernels(np.float32)
+
+    def step(self):
+        """Returns (seconds of the G-member step, seconds of the lm_rows LM head)."""
+        t0 = time.perf_counter()
+        xr = self.ret(self.state, self.layers, self.x, self.p, self.pool)
+        y = self.fwd(self.p, self.layers, xr, self.pool)
+        self.upd(self.state, self.layers, y[:, -self.cfg.num_mem_tokens:, :], self.p, self.pool)
+        t1 = time.perf_counter()
+        self.armt.gemm(np.ascontiguousarray(y[0, :self.lm_rows]), self.U)
+        return t1 - t0, time.perf_counter() - t1
+
+    def extrapolate(self, cfg, S: int, t_cells: float, t_lm: float) -> dict:
+        """Forward seconds for S segments of ``cfg``: every cell at the measured
+        full-group throughput (a lower bound on the reference's diagonal-run time:
+        ramp steps with fewer members than cores are slower per cell) + S heads."""
+        rate_cells = self.G * cell_flops(self.cfg) / t_cells
+        rate_lm = 2.0 * self.lm_rows * cfg.d_model * cfg.vocab_size / t_lm
+        t_cell = cell_flops(cfg) / rate_cells
+        t_head = 2.0 * cfg.segment_size * cfg.d_model * cfg.vocab_size / rate_lm
+        return {"total_s": S * cfg.n_layers * t_cell + S * t_head, "t_cell": t_cell, "t_head": t_head,
+                "gflops_cells": rate_cells / 1e9, "gflops_lm": rate_lm / 1e9}
+
+    def describe(self) -> str:
+        return (f"reference armt (baseline/_ref, numba f32) on {self.cores} host threads ({cpu_model()}): per step "
+                f"one diagonal step of {self.G} full-width cells (segment {self.seg} + "
+                f"{self.cfg.num_mem_tokens} memory tokens, WorkerPool({self.cores})) + a {self.lm_rows}-row LM head "
+                f"at V={self.V}; extrapolated by FLOPs to full cells/heads, every cell at full-group throughput")
+
+
 def reference_arm(args, rank, world):
-    """The reference's CPU path on this host: the oracle port (NumPy/BLAS f32, all
-    threads) timed on full-width cells of the requested config + one LM head and
-    extrapolated over the schedule; weights for a 2-layer sample (per-cell cost is
-    layer-independent). Rank 0 only."""
+    """``--impl reference``: the reference's own CPU implementation (numba, all host
+    threads) on bounded samples of the requested workload; rank 0 only. Falls
+    back to the NumPy/BLAS oracle port when baseline/_ref is absent."""
     if rank != 0:
         return 0
-    from dataclasses import replace as _replace
     from paper_2506_05229_b200 import ModelConfig
     model, n_cfg, desc = CONFIGS[args.config]
-    cfg = ModelConfig(**model, eps_assoc=EPS_ASSOC, seed=0)
+    eps = args.eps if args.eps is not None else (EPS_C5 if args.config == "c5" else EPS_ASSOC)
+    cfg = ModelConfig(**model, eps_assoc=eps, seed=0)
     n = args.tokens or n_cfg
     if args.segments is not None:
         n = args.segments * cfg.segment_size
     S = -(-n // cfg.segment_size)
-    sample = _replace(cfg, n_layers=min(2, cfg.n_layers))
-    w = make_weights(sample)
-    rates, totals = [], []
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_rate(w, sample, S, budget_s=4.0, max_cells=4, n_layers=cfg.n_layers)
-        if i >= args.warmup:
-            totals.append(r["total_s"])
-            rates.append(n / r["total_s"])
+    base = shared_config(args, cfg, n, S, desc)
+    try:
+        ref = ReferenceCells(model, eps)
+    except ImportError as exc:
+        ref = None
+        why = f"baseline/_ref not importable ({exc}); oracle port instead"
+    rates, walls = [], []
+    if ref is not None:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            tc, tl = ref.step()
+            walls.append(time.perf_counter() - t0)
+            if i >= args.warmup:
+                rates.append(n / ref.extrapolate(cfg, S, tc, tl)["total_s"])
+        kind, cores, sample = "reference", ref.cores, ref.describe()
+    else:
+        from dataclasses import replace as _replace
+        sample_cfg = _replace(cfg, n_layers=min(2, cfg.n_layers))
+        w = make_weights(sample_cfg)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            r = cpu_oracle_rate(w, sample_cfg, S, budget_s=4.0, max_cells=4, n_layers=cfg.n_layers)
+            walls.append(time.perf_counter() - t0)
+            if i >= args.warmup:
+                rates.append(n / r["total_s"])
+        kind, cores, sample = "port", r["threads"], f"{why}: numpy/BLAS f32 cells + 1 LM head, extrapolated"
     value = statistics.mean(rates)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(totals),
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.mean(walls[args.warmup:]),
+            "ms_per_step_note": "measured wall time of one bounded sample step; value extrapolates the "
+                                "sample's measured throughput to the whole forward",
+            "extrapolated_forward_s": n / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded reference init, cli token convention)",
-            "config": {"workload": f"{desc}, {n} tokens",
-                       "schedule": "oracle cells (schedule-invariant per-cell cost)"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-                             "sample": f"per step: {r['cells']} full-width cells (retrieve+block+fold) + 1 "
-                                       f"segment LM head in numpy/BLAS f32, extrapolated to {S}x{cfg.n_layers} "
-                                       f"cells + {S} heads"},
+            "config": base,
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def shared_config(args, cfg, n, S, desc) -> dict:
+    """The workload identity both arms report (identical dicts for the same flags)."""
+    return {"workload": f"{desc}, {n} tokens", "schedule": args.schedule, "segments": S,
+            "init": args.init or ("device" if args.config == "c5" else "reference"),
+            "eps_assoc": cfg.eps_assoc, "output": "fused NLL (no logits)" if (args.scoring or args.config == "c4")
+            else "logits", "l2": "inputs > L2 (3.3 GB bf16 weights, 33.6 GB logits); no flush"}
 
 
 # ---------------------------------------------------------------------------- device arm
@@ -427,12 +527,26 @@ def device_arm(args, rank, world):
 
     if rank != 0:
         return 0
-    cpu = None
+    cpu = cpu_port = None
     if world == 1 and not args.no_cpu_baseline and init == "reference":
-        r = cpu_oracle_rate(w, cfg, S)
-        cpu = {"value": n / r["total_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-               "sample": f"{r['cells']} full-width C2 cells (retrieve+block+fold) + 1 segment LM head, numpy/BLAS "
-                         f"f32 oracle ({r['sample_s']:.1f} s), extrapolated to {S}x{cfg.n_layers} cells + {S} heads"}
+        # the reference's own numba path (baseline/_ref) on the host cores: one warm-up and one measured step
+        try:
+            ref = ReferenceCells(model, eps)
+            ref.step()
+            tc, tl = ref.step()
+            ex = ref.extrapolate(cfg, S, tc, tl)
+            cpu = {"value": n / ex["total_s"], "unit": "tokens/s", "cores": ref.cores, "kind": "reference",
+                   "sample": ref.describe() + f" ({tc + tl:.1f} s measured; {ex['gflops_cells']:.1f} GFLOP/s on cells, "
+                             f"{ex['gflops_lm']:.1f} GFLOP/s LM head)", "cpu_model": cpu_model()}
+            del ref
+        except ImportError:
+            pass
+        r = cpu_oracle_rate(w, cfg, S, budget_s=8.0)
+        cpu_port = {"value": n / r["total_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                    "sample": f"{r['cells']} full-width C2 cells (retrieve+block+fold) + 1 segment LM head, "
+                              f"numpy/BLAS f32 oracle ({r['sample_s']:.1f} s), extrapolated to {S}x{cfg.n_layers} "
+                              f"cells + {S} heads"}
+        cpu = cpu or cpu_port
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -440,14 +554,12 @@ def device_arm(args, rank, world):
         "data": (f"synthetic: reference seeded init (seed 0, w_v_mem/32, eps_assoc {eps:g}), cli token convention"
                  if init == "reference" else
                  f"synthetic: seeded device init with the reference's scales (w_v_mem/32, eps_assoc {eps:g}), cli tokens"),
-        "config": {"workload": f"{desc}, {n} tokens", "schedule": args.schedule, "segments": S,
-                   "init": init, "output": "fused NLL (no logits)" if scoring_value else "bf16 logits",
-                   "parallelism": f"layer-shard{world}" if world > 1 else "single",
-                   "l2": "inputs > L2 (3.3 GB bf16 weights, 33.6 GB logits); no flush",
-                   "timing": "CUDA events around one CUDA-graph replay of the whole forward, max over ranks",
-                   "whole_step_tflops": step_tflops,
-                   "whole_step_frac_of_sustained": step_tflops / peaks.get("bf16_tflops_sustained", peak),
-                   "setup_s": setup_s},
+        "config": shared_config(args, cfg, n, S, desc),
+        "parallelism": f"layer-shard{world}" if world > 1 else "single",
+        "timing": "CUDA events around one CUDA-graph replay of the whole forward, max over ranks",
+        "whole_step_tflops": step_tflops,
+        "whole_step_frac_of_sustained": step_tflops / peaks.get("bf16_tflops_sustained", peak),
+        "setup_s": setup_s,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": (traffic or {}).get("bytes"),
@@ -457,6 +569,7 @@ def device_arm(args, rank, world):
                                f"{gu_flops / 1e12:.3f} TFLOP/launch, {n_probe} launches/step",
                      "peak_kind": f"{peak_kind} bf16_tflops_sustained"},
         "cpu_baseline": cpu,
+        "cpu_baseline_port": cpu_port if cpu is not cpu_port else None,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(n * 8),
                 "d2h_bytes_per_step": int((n - 1) * 4),
                 "api": "Session(scoring=True).nll: pinned ids in, per-token NLL out (LM-head fused NLL)"
