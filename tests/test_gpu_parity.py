@@ -363,3 +363,36 @@ def test_reference_written_container_drives_the_device(dtype):
     logits, _ = run_diagonal(w, cfg, g["tokens"], dtype=dtype, state=state)
     assert relative_error(logits, g["logits_f64"]) < TOL[dtype]
     assert relative_error(state.A.cpu().numpy(), g["A_f64"]) < TOL[dtype]
+
+
+def test_dropin_calls_reuse_prepared_weights_and_replay_one_graph(monkeypatch):
+    """run_diagonal(GroupedWeights, ...) as a reference user calls it: weights
+    are prepared once per weight object, the first call of a length runs
+    eagerly and later calls replay one captured graph of the whole schedule —
+    bitwise the eager result, with the caller's memory state carried across
+    calls like the eager path; an in-place weight edit is picked up."""
+    from paper_2506_05229_b200 import executors as X
+    X.clear_caches()
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    w = conditioned_weights(cfg)
+    tokens = cli_tokens(cfg, 5 * cfg.segment_size - 7)
+    calls = []
+    real = X.prepare_weights
+    monkeypatch.setattr(X, "prepare_weights", lambda *a, **k: calls.append(1) or real(*a, **k))
+    st_e, st_g = MemoryState.fresh(cfg), MemoryState.fresh(cfg)
+    eager = [run_diagonal(w, cfg, tokens, state=st_e, graph=False)[0] for _ in range(3)]
+    assert len(calls) == 1
+    X.clear_caches()
+    got = [run_diagonal(w, cfg, tokens, state=st_g)[0] for _ in range(3)]
+    assert len(calls) == 2
+    run = next(iter(X._RUN_CACHE.values()))
+    assert run.runner.graph is not None and run.calls == 3
+    for a, b in zip(eager, got):
+        assert np.array_equal(a, b)
+    assert torch.equal(st_e.A, st_g.A) and torch.equal(st_e.z, st_g.z)
+    assert np.array_equal(st_e.updates, st_g.updates)
+    w.wo[0] *= 0.5
+    changed, _ = run_diagonal(w, cfg, tokens)
+    assert len(calls) == 3
+    assert not np.array_equal(changed, eager[0])   # fresh state both times: only the weights differ
+    X.clear_caches()
