@@ -50,9 +50,12 @@ typedef enum {
   ARMT_EPI_LSE = 5,       /* no C: per row and N-tile (max, sum exp) of acc in base-2 units into
                              lse_part[row*lse_ld + nb] (float2), and acc[row][targets[row]] into
                              lse_tgt[row] -- the fused next-token NLL of the LM head */
-  ARMT_EPI_DPFP = 6       /* acc = q (M x N, N = d_mem <= 64): C = bf16 DPFP_nu(q) (ldc >= 2*nu*N) and
+  ARMT_EPI_DPFP = 6,      /* acc = q (M x N, N = d_mem <= 64): C = bf16 DPFP_nu(q) (ldc >= 2*nu*N) and
                              den[g*den_stride + m] = DPFP(q) . z[e_index[g]] (z rows of 2*nu*N floats)
                              armt/memory.py:34-45,137-147 -- retrieval's feature map fused into q-proj */
+  ARMT_EPI_FOLDR = 7      /* fold-internal (armt_mem_fold_tc): acc = P^T = A0 Phi^T (M = d rows, N = n_mem
+                             token columns); C row r = bf16 [V hi | P hi | V lo | P lo],
+                             c2_split = segment width, V[r][i] = R[i*ldr + r] (value rows, token-major) */
 } ArmtEpilogue;
 
 /* Members of one grouped launch: member g runs slot[g] against layer[g]. */
@@ -77,7 +80,7 @@ typedef struct {
   int epilogue;                         /* ArmtEpilogue */
   const float* R; long long ldr, r_stride;     /* RESIDUAL/RETRIEVE input, indexed by c_slot */
   void* C2; long long ldc2, c2_stride;         /* RESIDUAL: optional bf16 copy, indexed by c_slot */
-  int c2_split;                         /* >0: C2 gets [hi | lo | hi] bf16 split of C at cols n, n+s, n+2s */
+  int c2_split;                         /* >0: C2 gets the [hi | lo] bf16 split of C at cols n, n+s */
   /* fused RMSNorm (bf16 path): RESIDUAL/RETRIEVE epilogues write sum(C^2) of each row per
    * 64-column block to ssq_out[g*ssq_stride + m*ssq_np + n/64]; ROPE/SWIGLU epilogues scale
    * the accumulator row by 1/sqrt(sum_p ssq_in[g*ssq_stride + m*ssq_np + p]/norm_d + norm_eps),
@@ -93,6 +96,9 @@ typedef struct {
   int max_ctas;                         /* bf16 engine: cap on resident CTAs (0 = one per SM); lets a
                                            launch leave SMs free for a concurrent stream */
   const float* z; int nu;               /* DPFP: memory normaliser rows and feature-map order */
+  int a_kwrap, b_kwrap;                 /* >0: operand K columns [w, K) are read from [0, K - w) (a bf16x3
+                                           operand stores [hi | lo] once and reuses hi as its third part);
+                                           multiples of 64; 0 = plain */
   int a_slot[ARMT_MAX_MEMBERS];
   int b_index[ARMT_MAX_MEMBERS];
   int c_slot[ARMT_MAX_MEMBERS];
@@ -155,11 +161,11 @@ int armt_mem_fold(const ArmtMembers* mem, const float* kvb, long long ld_kvb,
                   float eps, void* ws, void* stream);
 long long armt_fold_workspace_bytes(int G, int n_mem, int d_phi);
 
-/* Tensor-core form of the same fold for the bf16 path (chunked delta rule:
- * U = L^{-1} R with L = I + diag(c) tril(Phi Phi^T, -1), A += U^T Phi; two grouped
- * tcgen05 GEMMs on bf16x3-split operands). `memop` (L, armt_memop_rows(d, M), 3*P) bf16,
- * P = d_phi rounded up to 8, holds per layer the [hi|lo|hi] split of A (rows 0..d-1),
- * of z (row d) and of the member's phi (rows d+8..); retrieval reads its hi part.
+/* Tensor-core form of the same fold for the bf16 path (chunked delta rule: with
+ * L = I + diag(c) tril(Phi Phi^T, -1) and W = L^{-T} Phi, A += [V^T | (A Phi^T)^T-rows] [diag(beta) W ;
+ * -diag(c) W]; grouped tcgen05 GEMMs on bf16x3-split operands, the chain and L^{-1} in smem).
+ * `memop` (L, armt_memop_rows(d, M), 2*P) bf16, P = d_phi rounded up to 32, holds per layer
+ * the [hi|lo] split of A (rows 0..d-1) and of z (row d); retrieval reads its hi part.
  * ws: armt_fold_tc_workspace_bytes(G, M, d, d_phi) bytes, zero-initialised once. */
 int armt_mem_fold_tc(const ArmtMembers* mem, const float* kvb, long long ld_kvb,
                      long long kvb_stride, int v_off, int k_off, int b_off, float* A, float* z,

@@ -59,6 +59,7 @@ class ArmtGemmArgs(ctypes.Structure):
         ("swiglu_block", _I),
         ("max_ctas", _I),
         ("z", _P), ("nu", _I),
+        ("a_kwrap", _I), ("b_kwrap", _I),
         ("a_slot", _I * MAX_MEMBERS),
         ("b_index", _I * MAX_MEMBERS),
         ("c_slot", _I * MAX_MEMBERS),

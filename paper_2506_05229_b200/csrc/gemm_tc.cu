@@ -63,14 +63,19 @@ struct Params {
   short c_slot[ARMT_MAX_MEMBERS];
   short e_index[ARMT_MAX_MEMBERS];
   const float* z; int nu;
+  int a_kwrap, b_kwrap;   // operand K-column reuse (see ArmtGemmArgs)
 };
 
 // PAIR: a 2-CTA cluster computes a 256 x BN tile with one cta_group::2 MMA per K
 // step; each CTA holds its 128 A rows and half (BN/2) of the B rows, so per-CTA
 // operand traffic per flop drops by a third and 6 stages fit in the same smem.
-template <int BN, bool PAIR = false> struct Cfg {
+// TMAE: TMA epilogue for the short-K residual / retrieve GEMMs — the residual tile is
+// TMA-loaded into swizzled smem ahead of the accumulator, and the f32 result and its bf16
+// copy leave by TMA stores; it trades mainloop stages for 16 KB of epilogue buffers per warp.
+template <int BN, bool PAIR = false, bool TMAE = false> struct Cfg {
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
-  static constexpr int STAGES = PAIR ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  static constexpr int STAGES = TMAE ? (PAIR ? 3 : (BN == 256 ? 2 : (BN == 128 ? 3 : 4)))
+                                     : (PAIR ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -79,18 +84,30 @@ template <int BN, bool PAIR = false> struct Cfg {
   // residual/retrieve epilogues: one 32 x 32 f32 transpose tile per epilogue warp
   static constexpr int XPOSE_BYTES = 8 * 32 * 32 * 4;
   static constexpr int SMEM_XPOSE = SMEM_BYTES + XPOSE_BYTES;
+  // TMAE: per epilogue warp 2 f32 tiles (32 x 32, 128B-swizzled) + 4 bf16 tiles (32 x 32, 64B-swizzled)
+  static constexpr int EW_BYTES = 2 * 4096 + 4 * 2048;
+  static constexpr int SMEM_TMAE = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 8 * EW_BYTES;
 };
 
 using namespace tcx;
 
 // ---------------------------------------------------------------- epilogues
-enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4, E_LSE = 5, E_DPFP = 6 };
+enum : int { E_STORE = 0, E_RESIDUAL = 1, E_RETRIEVE = 2, E_SWIGLU = 3, E_ROPE = 4, E_LSE = 5, E_DPFP = 6,
+             E_FOLDR = 7 };
 
 __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) = 0
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float fast_rcp(float x) {  // MUFU.RCP
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+#ifndef ARMT_SWIGLU_FAST
+#define ARMT_SWIGLU_FAST 1
+#endif
 
 // Store 32 consecutive values of one row starting at column n0 (< N).
 __device__ __forceinline__ void store_row32(void* base, int dtype, long long off, int n0, int N,
@@ -188,12 +205,14 @@ __device__ unsigned long long g_gemm_prof[8];
 // (m, n), (m+1, n) shares the B tile and (m, n), (m, n+1) the A tile; each CTA loads
 // its own unshared operand and HALF of the shared one, multicast into both CTAs'
 // smem, so per-CTA L2->SM operand traffic drops by a third with no tile padding.
-template <int BN, int EPI, int DH, bool PAIR, bool MC = false>
+template <int BN, int EPI, int DH, bool PAIR, bool MC = false, bool TMAE = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-            const __grid_constant__ Params p) {
-  using C = Cfg<BN, PAIR>;
+            const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC,
+            const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ Params p) {
+  using C = Cfg<BN, PAIR, TMAE>;
+  static_assert(!TMAE || EPI == E_RESIDUAL || EPI == E_RETRIEVE, "TMA epilogue: residual / retrieve only");
   constexpr bool CLUSTER = PAIR || MC;
   constexpr int TM = PAIR ? 2 * BM : BM;   // rows per tile (per pair)
   constexpr int STAGES = C::STAGES;
@@ -214,6 +233,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* tq_full = bars + 2 * STAGES + 5;
   uint64_t* tq_empty = tq_full + QD;
   volatile int* tq_ids = reinterpret_cast<volatile int*>(tq_empty + QD);
+  // TMAE: two residual-tile barriers per epilogue warp, then the per-warp tile buffers
+  uint64_t* rbar = bars + 2 * STAGES + 5 + 2 * QD + 4;
+  uint8_t* ebuf = smem + STAGES * C::STAGE_BYTES + 1024;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -229,6 +251,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], MC ? 2 : 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], PAIR ? 8 : 4); }
     for (int i = 0; i < QD; ++i) { mbar_init(&tq_full[i], 1); mbar_init(&tq_empty[i], 5); }
+    if constexpr (TMAE)
+      for (int i = 0; i < 16; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -310,29 +334,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_wait(&empty[stage], phase ^ 1);
             w_empty += clock64() - t0;
           }
+          // K coordinates: a bf16x3 operand stored as [hi | lo] re-reads hi as its third part
+          const int ka = (p.a_kwrap > 0 && kb * BK >= p.a_kwrap) ? kb * BK - p.a_kwrap : kb * BK;
+          const int kbb = (p.b_kwrap > 0 && kb * BK >= p.b_kwrap) ? kb * BK - p.b_kwrap : kb * BK;
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (PAIR) {
             // both CTAs' bytes complete on the leader's full barrier; the leader arms it
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             const uint32_t lbar = mapa_shared(&full[stage], 0);
-            tma_load_3d_pair(sA + stage * C::A_BYTES, &tmA, lbar, kb * BK, a_row, a_slot);
-            tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, lbar, kb * BK, b_row, b_idx);
+            tma_load_3d_pair(sA + stage * C::A_BYTES, &tmA, lbar, ka, a_row, a_slot);
+            tma_load_3d_pair(sB + stage * C::B_BYTES, &tmB, lbar, kbb, b_row, b_idx);
           } else if constexpr (MC) {
             // own operand unicast; half of the shared one multicast to both CTAs
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
             if (!share_a) {
-              tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
-              tma_load_3d_mc(sB + stage * C::B_BYTES + rank * (C::B_BYTES / 2), &tmB2, &full[stage], kb * BK,
+              tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], ka, a_row, a_slot);
+              tma_load_3d_mc(sB + stage * C::B_BYTES + rank * (C::B_BYTES / 2), &tmB2, &full[stage], kbb,
                              b_row + (int)rank * (BN / 2), b_idx, (uint16_t)3);
             } else {
-              tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, b_row, b_idx);
-              tma_load_3d_mc(sA + stage * C::A_BYTES + rank * (C::A_BYTES / 2), &tmA2, &full[stage], kb * BK,
+              tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kbb, b_row, b_idx);
+              tma_load_3d_mc(sA + stage * C::A_BYTES + rank * (C::A_BYTES / 2), &tmA2, &full[stage], ka,
                              a_row + (int)rank * (BM / 2), a_slot, (uint16_t)3);
             }
           } else {
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, a_slot);
-            tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, b_row, b_idx);
+            tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], ka, a_row, a_slot);
+            tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], kbb, b_row, b_idx);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -404,6 +431,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int eg = (warp - 4) >> 2;
     const int acc = eg;
     uint32_t acc_phase = 0;
+    uint32_t rph = 0;   // TMAE: parity of this warp's two residual-tile barriers
     int qk = eg;
     auto first = [&]() { const int t = tile0 + eg * tstep; return t < p.num_tiles ? t : -1; };
     for (int tile = dyn ? tq_pop(qk, true) : first(); tile >= 0;
@@ -413,6 +441,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int row = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32 + lane;
       const bool live = row < p.M;
       const int c_slot = p.c_slot[g];
+      // TMAE: chunks of this tile inside N, and the first two residual tiles requested now
+      // (they do not depend on the MMA, so they land while the mainloop runs)
+      const int ncv = TMAE ? min(BN / 32, (p.N - nb * BN + 31) / 32) : 0;
+      uint8_t* wbuf = ebuf + (warp - 4) * C::EW_BYTES;
+      if constexpr (TMAE) {
+        if (lane == 0) {
+          bulk_wait_read0();   // the previous tile's stores have left these buffers
+          const int wr0 = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32;
+          for (int c = 0; c < 2 && c < ncv; ++c) {
+            mbar_expect_tx(&rbar[2 * (warp - 4) + c], 4096);
+            tma_load_3d(wbuf + c * 4096, &tmR, &rbar[2 * (warp - 4) + c], nb * BN + 32 * c, wr0, c_slot);
+          }
+        }
+      }
       if (p.prof && lane == 0) {
         const long long t0 = clock64();
         mbar_wait_sleep(&tfull[acc], acc_phase);
@@ -488,6 +530,53 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           }
         }
         if (live) const_cast<float*>(p.den)[(long long)g * p.den_stride + row] = dacc;  // (RETRIEVE reads den)
+      } else if constexpr (EPI == E_FOLDR) {
+        // The fold's transposed projection (memory_tc.cu): acc[r][i] = (A0 phi_i)[r]. Row r of
+        // member g's output, segments of seg = c2_split token columns:
+        //   [V hi | P hi | V lo | P lo],  V[r][i] = v_i[r] (R: token-major value rows)
+        // i.e. the bf16x3 A operand of the fold's update GEMM A_M = A0 + [V^T | P^T] [Y ; Z]^T,
+        // whose third part [V hi | P hi] is re-read from the first through a K wrap.
+        const int seg = p.c2_split;
+        __nv_bfloat16* cb = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride;
+        const float* vb = p.R + (long long)c_slot * p.r_stride;
+        uint4* tb = reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128;
+        const int wrow0 = row - lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int n0 = nb * BN + c0;
+          if (n0 >= seg) break;  // warp-uniform
+          float v[32];
+          __syncwarp();
+          tmem_ld32(tbase + c0, v);
+          float vv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) vv[j] = (live && n0 + j < p.N) ? vb[(long long)(n0 + j) * p.ldr + row] : 0.f;
+          float hi[32], lo[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            hi[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+            lo[j] = v[j] - hi[j];
+            v[j] = __bfloat162float(__float2bfloat16_rn(vv[j]));   // V hi
+            vv[j] = vv[j] - v[j];                                  // V lo
+          }
+          if (n0 + 32 <= seg) {  // warp-uniform: whole 32-column chunks through the smem transpose
+            store_chunk_bf16_coalesced(tb, lane, v, cb, p.ldc, wrow0, p.M, n0);
+            store_chunk_bf16_coalesced(tb, lane, hi, cb, p.ldc, wrow0, p.M, seg + n0);
+            store_chunk_bf16_coalesced(tb, lane, vv, cb, p.ldc, wrow0, p.M, 2 * seg + n0);
+            store_chunk_bf16_coalesced(tb, lane, lo, cb, p.ldc, wrow0, p.M, 3 * seg + n0);
+          } else if (live) {
+            __nv_bfloat16* o = cb + (long long)row * p.ldc + n0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (n0 + j < seg) {
+                o[j] = __float2bfloat16_rn(v[j]);
+                o[seg + j] = __float2bfloat16_rn(hi[j]);
+                o[2 * seg + j] = __float2bfloat16_rn(vv[j]);
+                o[3 * seg + j] = __float2bfloat16_rn(lo[j]);
+              }
+            }
+          }
+        }
       } else if constexpr (EPI == E_LSE) {
         // fused next-token NLL: online (max, sum 2^x) of the row's logits in base 2
         constexpr float LOG2E = 1.4426950408889634f;
@@ -529,7 +618,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float gv = gte[j] * rs;
+#if ARMT_SWIGLU_FAST
+            // silu(g) = g / (1 + 2^(-g log2 e)): MUFU.EX2 + MUFU.RCP (approximate, ~2 ulp, far
+            // below the bf16 rounding of the output) instead of the IEEE reciprocal sequence
+            gte[j] = gv * fast_rcp(1.f + fast_exp2(-1.4426950408889634f * gv)) * (up[j] * rs);
+#else
             gte[j] = gv * __frcp_rn(1.f + __expf(-gv)) * (up[j] * rs);
+#endif
           }
           if (p.cst && out_n0 + c0 + 32 <= p.N / 2) {
             store_chunk_bf16_coalesced(reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128, lane, gte,
@@ -605,6 +700,81 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           rden = 1.f / den;
         }
         if constexpr (EPI == E_RESIDUAL || EPI == E_RETRIEVE) {
+          if constexpr (TMAE) {
+            // lane = row. Residual tile (f32, 128B swizzle: 16-byte chunk k of row r at k ^ (r & 7))
+            // -> o = R + f(acc) written back in place -> TMA store; bf16 copy (64B swizzle: chunk k
+            // of row r at k ^ ((r >> 1) & 3)) -> TMA store. Row sums of squares per 64 columns in the
+            // same order as the xpose path (4-column fma chains, then a fixed pairwise tree).
+            const int wrow0 = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32;
+            const int wi = warp - 4;
+            const bool split = p.c2_split > 0;
+            float sq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sq[k] = 0.f;
+#pragma unroll 1
+            for (int c = 0; c < ncv; ++c) {
+              const int b = c & 1, c0 = 32 * c, n0 = nb * BN + c0;
+              float v[32];
+              __syncwarp();
+              tmem_ld32(tbase + c0, v);
+              mbar_wait(&rbar[2 * wi + b], (rph >> b) & 1);
+              rph ^= 1u << b;
+              float4* fb = reinterpret_cast<float4*>(wbuf + b * 4096) + lane * 8;
+              uint4* hb = reinterpret_cast<uint4*>(wbuf + 8192 + b * 2048) + lane * 4;
+              uint4* lb = reinterpret_cast<uint4*>(wbuf + 8192 + (2 + b) * 2048) + lane * 4;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float4 r4 = fb[k ^ (lane & 7)];
+                float a0 = v[4 * k], a1 = v[4 * k + 1], a2 = v[4 * k + 2], a3 = v[4 * k + 3];
+                if constexpr (EPI == E_RETRIEVE) {
+                  a0 = guarded ? 0.f : a0 * rden; a1 = guarded ? 0.f : a1 * rden;
+                  a2 = guarded ? 0.f : a2 * rden; a3 = guarded ? 0.f : a3 * rden;
+                }
+                float4 o;
+                o.x = r4.x + a0; o.y = r4.y + a1; o.z = r4.z + a2; o.w = r4.w + a3;
+                fb[k ^ (lane & 7)] = o;
+                sq[k] = fmaf(o.w, o.w, fmaf(o.z, o.z, fmaf(o.y, o.y, fmaf(o.x, o.x, sq[k]))));
+                v[4 * k] = o.x; v[4 * k + 1] = o.y; v[4 * k + 2] = o.z; v[4 * k + 3] = o.w;
+              }
+              if (p.C2 != nullptr) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int pk = k ^ ((lane >> 1) & 3);
+                  hb[pk] = make_uint4(pack_bf16x2(v[8 * k], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
+                                      pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+                  if (split) {
+                    float l[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) l[u] = v[8 * k + u] - __bfloat162float(__float2bfloat16_rn(v[8 * k + u]));
+                    lb[pk] = make_uint4(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3]),
+                                        pack_bf16x2(l[4], l[5]), pack_bf16x2(l[6], l[7]));
+                  }
+                }
+              }
+              fence_async_smem();   // generic-proxy smem writes -> visible to the TMA engine
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&tmC, wbuf + b * 4096, n0, wrow0, c_slot);
+                if (p.C2 != nullptr) {
+                  tma_store_3d(&tmC2, wbuf + 8192 + b * 2048, n0, wrow0, c_slot);
+                  if (split) tma_store_3d(&tmC2, wbuf + 8192 + (2 + b) * 2048, n0 + p.c2_split, wrow0, c_slot);
+                }
+                bulk_commit();
+                if (c + 2 < ncv) {   // refill this buffer pair once the stores have read it
+                  bulk_wait_read0();
+                  mbar_expect_tx(&rbar[2 * wi + b], 4096);
+                  tma_load_3d(wbuf + b * 4096, &tmR, &rbar[2 * wi + b], n0 + 64, wrow0, c_slot);
+                }
+              }
+              if (p.ssq_out != nullptr && ((n0 & 63) == 32 || n0 + 32 >= p.N)) {
+                const float t = ((sq[0] + sq[1]) + (sq[2] + sq[3])) + ((sq[4] + sq[5]) + (sq[6] + sq[7]));
+                if (live) p.ssq_out[(long long)g * p.ssq_stride + (long long)row * p.ssq_np + (n0 >> 6)] = t;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sq[k] = 0.f;
+              }
+            }
+            goto epi_done;
+          }
           if (p.xpose) {
             // Each 32 x 32 chunk: TMEM -> registers (lane = row) -> swizzled smem tile ->
             // registers with lane = (row group, 4-column group): the residual load and the
@@ -656,7 +826,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     const uint2 hi = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
                     *reinterpret_cast<uint2*>(q) = hi;
                     if (p.c2_split > 0) {
-                      *reinterpret_cast<uint2*>(q + 2 * p.c2_split) = hi;
                       const uint2 lo = make_uint2(
                           pack_bf16x2(o.x - __bfloat162float(__float2bfloat16_rn(o.x)),
                                       o.y - __bfloat162float(__float2bfloat16_rn(o.y))),
@@ -725,7 +894,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if (p.C2 != nullptr) {
               const long long off2 = (long long)c_slot * p.c2_stride + (long long)row * p.ldc2;
               if (p.c2_split > 0) {
-                // bf16x3 operand layout [hi | lo | hi]: v ~= hi + lo to ~2^-16 relative
+                // bf16x3 operand layout [hi | lo] (hi re-read as the third part through a K wrap):
+                // v ~= hi + lo to ~2^-16 relative
                 float hi[32], lo[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
@@ -734,7 +904,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
                 store_row32(p.C2, ARMT_BF16, off2, n0, p.N, p.ldc2, hi);
                 store_row32(p.C2, ARMT_BF16, off2 + p.c2_split, n0, p.N, p.ldc2, lo);
-                store_row32(p.C2, ARMT_BF16, off2 + 2 * p.c2_split, n0, p.N, p.ldc2, hi);
               } else {
                 store_row32(p.C2, ARMT_BF16, off2, n0, p.N, p.ldc2, v);
               }
@@ -755,6 +924,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
   }
 
+  if constexpr (TMAE) {
+    if (warp >= 4 && lane == 0) bulk_wait0();   // TMA stores complete before the CTA's smem goes away
+  }
   __syncwarp();
   tc_fence_before();
   __syncthreads();
@@ -805,12 +977,33 @@ static int make_map(CUtensorMap* map, const void* base, long long cols, long lon
   return ARMT_OK;
 }
 
-struct Maps { CUtensorMap a, b, a2, b2; };
+// Epilogue tile maps (TMAE): (cols, rows, batch) with a (32, 32, 1) box; f32 tiles 128B-swizzled,
+// bf16 tiles 64B-swizzled (the swizzles the epilogue's row-per-lane smem accesses assume).
+static int make_epi_map(CUtensorMap* map, bool f32, const void* base, long long cols, long long rows,
+                        long long batches, long long ld, long long batch_stride) {
+  auto encode = get_encode();
+  ARMT_REQUIRE(encode != nullptr, ARMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const long long es = f32 ? 4 : 2;
+  if (batches == 1) batch_stride = rows * ld;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batches};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * es), (cuuint64_t)(batch_stride * es)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ARMT_REQUIRE(r == CUDA_SUCCESS, ARMT_ERR_DIM, "epilogue tensor map failed (%d)", (int)r);
+  return ARMT_OK;
+}
 
-template <int BN, int EPI, int DH, bool PAIR, bool MC>
+struct Maps { CUtensorMap a, b, a2, b2, r, c, c2; };
+
+template <int BN, int EPI, int DH, bool PAIR, bool MC, bool TMAE = false>
 static int launch(const Maps& m, const Params& p, cudaStream_t s) {
-  auto kern = gemm_kernel<BN, EPI, DH, PAIR, MC>;
-  constexpr int smem = (EPI == E_LSE) ? Cfg<BN, PAIR>::SMEM_BYTES : Cfg<BN, PAIR>::SMEM_XPOSE;
+  auto kern = gemm_kernel<BN, EPI, DH, PAIR, MC, TMAE>;
+  constexpr int smem = TMAE ? Cfg<BN, PAIR, true>::SMEM_TMAE
+                            : (EPI == E_LSE) ? Cfg<BN, PAIR>::SMEM_BYTES : Cfg<BN, PAIR>::SMEM_XPOSE;
   static_assert(smem <= 227 * 1024, "GEMM shared memory budget");
   static bool attr_done = false;
   if (!attr_done) {
@@ -837,7 +1030,7 @@ static int launch(const Maps& m, const Params& p, cudaStream_t s) {
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, m.r, m.c, m.c2, p);
     ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 cluster gemm launch: %s", cudaGetErrorString(e));
   } else {
     const int grid = p.num_tiles < cap ? p.num_tiles : cap;
@@ -852,7 +1045,7 @@ static int launch(const Maps& m, const Params& p, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.a2, m.b2, m.r, m.c, m.c2, p);
     ARMT_REQUIRE(e == cudaSuccess, ARMT_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   }
   ARMT_CHECK_LAUNCH("tcgen05 gemm launch");
@@ -863,6 +1056,7 @@ static int pick_bn(const ArmtGemmArgs& a) {
   if (a.epilogue == ARMT_EPI_SWIGLU) return 2 * a.swiglu_block;
   if (a.epilogue == ARMT_EPI_LSE) return 256;  // lse_ld = ceil(N / 256) partials per row
   if (a.epilogue == ARMT_EPI_DPFP) return 64;  // one tile holds a whole q row
+  if (a.epilogue == ARMT_EPI_FOLDR) return a.N <= 64 ? 64 : 128;  // token columns (n_mem <= 128)
   if (const char* f = getenv("ARMT_GEMM_BN")) {  // tests: force a tile width
     const int v = atoi(f);
     if ((v == 64 || v == 128 || v == 256) && (a.epilogue != ARMT_EPI_ROPE || (v >= 128 && v % a.head_dim == 0)))
@@ -893,11 +1087,15 @@ static int pick_bn(const ArmtGemmArgs& a) {
 
 template <int BN, bool PAIR, bool MC>
 static int dispatch_epi(const ArmtGemmArgs& a, const Maps& m, const Params& p,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool tmae) {
   switch (a.epilogue) {
     case ARMT_EPI_STORE: return launch<BN, E_STORE, 0, PAIR, MC>(m, p, s);
-    case ARMT_EPI_RESIDUAL: return launch<BN, E_RESIDUAL, 0, PAIR, MC>(m, p, s);
-    case ARMT_EPI_RETRIEVE: return launch<BN, E_RETRIEVE, 0, PAIR, MC>(m, p, s);
+    case ARMT_EPI_RESIDUAL:
+      if (tmae) return launch<BN, E_RESIDUAL, 0, PAIR, MC, true>(m, p, s);
+      return launch<BN, E_RESIDUAL, 0, PAIR, MC>(m, p, s);
+    case ARMT_EPI_RETRIEVE:
+      if (tmae) return launch<BN, E_RETRIEVE, 0, PAIR, MC, true>(m, p, s);
+      return launch<BN, E_RETRIEVE, 0, PAIR, MC>(m, p, s);
     case ARMT_EPI_LSE:
       if constexpr (BN == 256) return launch<BN, E_LSE, 0, PAIR, MC>(m, p, s);
       break;
@@ -913,6 +1111,9 @@ static int dispatch_epi(const ArmtGemmArgs& a, const Maps& m, const Params& p,
       break;
     case ARMT_EPI_SWIGLU:
       if constexpr (BN == 64 || BN == 256) return launch<BN, E_SWIGLU, 0, PAIR, MC>(m, p, s);
+      break;
+    case ARMT_EPI_FOLDR:
+      if constexpr ((BN == 64 || BN == 128) && !PAIR && !MC) return launch<BN, E_FOLDR, 0, false, false>(m, p, s);
       break;
     case ARMT_EPI_ROPE:
       if constexpr (BN >= 128) {
@@ -948,19 +1149,22 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     max_b = a.b_index[g] > max_b ? a.b_index[g] : max_b;
   }
   Maps maps;
-  int rc = make_map(&maps.a, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM);
+  // a wrapped operand physically holds its first kwrap columns only
+  const long long ka_cols = a.a_kwrap > 0 ? a.a_kwrap : a.K, kb_cols = a.b_kwrap > 0 ? a.b_kwrap : a.K;
+  int rc = make_map(&maps.a, a.A, ka_cols, a.M, max_a + 1, a.lda, a.a_stride, BM);
   if (rc) return rc;
-  rc = make_map(&maps.b, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, pair ? bn / 2 : bn);
+  rc = make_map(&maps.b, a.B, kb_cols, a.N, max_b + 1, a.ldb, a.b_stride, pair ? bn / 2 : bn);
   if (rc) return rc;
   if (mc) {   // half-tile boxes for the multicast halves of the shared operand
-    rc = make_map(&maps.a2, a.A, a.K, a.M, max_a + 1, a.lda, a.a_stride, BM / 2);
+    rc = make_map(&maps.a2, a.A, ka_cols, a.M, max_a + 1, a.lda, a.a_stride, BM / 2);
     if (rc) return rc;
-    rc = make_map(&maps.b2, a.B, a.K, a.N, max_b + 1, a.ldb, a.b_stride, bn / 2);
+    rc = make_map(&maps.b2, a.B, kb_cols, a.N, max_b + 1, a.ldb, a.b_stride, bn / 2);
     if (rc) return rc;
   } else {
     maps.a2 = maps.a;
     maps.b2 = maps.b;
   }
+  maps.r = maps.c = maps.c2 = maps.a;
 
   Params p;
   memset(&p, 0, sizeof(p));
@@ -1036,23 +1240,52 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     p.e_index[g] = (short)a.e_index[g];
   }
   p.z = a.z; p.nu = a.nu;
+  p.a_kwrap = a.a_kwrap; p.b_kwrap = a.b_kwrap;
+  // TMA epilogue for the short-K (epilogue-bound) residual / retrieve GEMMs: residual tiles
+  // TMA-loaded ahead of the accumulator, results TMA-stored (ARMT_GEMM_TMAE=0 disables)
+  bool tmae = false;
+  {
+    const char* te = getenv("ARMT_GEMM_TMAE");
+    const bool tmae_on = !(te && te[0] == '0');
+    const bool heavy = a.epilogue == ARMT_EPI_RESIDUAL || a.epilogue == ARMT_EPI_RETRIEVE;
+    const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    tmae = tmae_on && heavy && p.xpose && a.K <= 2048 && a.c_dtype == ARMT_F32 && al16(a.C) && al16(a.R) &&
+           a.ldc % 4 == 0 && a.ldr % 4 == 0 && a.c_stride % 4 == 0 && a.r_stride % 4 == 0 &&
+           (a.C2 == nullptr || (al16(a.C2) && a.ldc2 % 8 == 0 && a.c2_stride % 8 == 0 && a.c2_split % 32 == 0));
+    if (tmae) {
+      int max_c = 0;
+      for (int g = 0; g < a.G; ++g) max_c = a.c_slot[g] > max_c ? a.c_slot[g] : max_c;
+      int rc2 = make_epi_map(&maps.r, true, a.R, a.N, m_end, max_c + 1, a.ldr, a.r_stride);
+      if (!rc2) rc2 = make_epi_map(&maps.c, true, a.C, a.N, m_end, max_c + 1, a.ldc, a.c_stride);
+      if (!rc2 && a.C2 != nullptr)
+        rc2 = make_epi_map(&maps.c2, false, a.C2, a.c2_split > 0 ? 2LL * a.c2_split : (long long)a.N, m_end,
+                           max_c + 1, a.ldc2, a.c2_stride);
+      if (rc2) return rc2;
+    }
+  }
   switch (bn) {
-    case 64: return dispatch_epi<64, false, false>(a, maps, p, s);
-    case 128: return dispatch_epi<128, false, false>(a, maps, p, s);
+    case 64: return dispatch_epi<64, false, false>(a, maps, p, s, tmae);
+    case 128: return dispatch_epi<128, false, false>(a, maps, p, s, tmae);
     case 256:
-      if (pair) return dispatch_epi<256, true, false>(a, maps, p, s);
-      if (mc) return dispatch_epi<256, false, true>(a, maps, p, s);
-      return dispatch_epi<256, false, false>(a, maps, p, s);
+      if (pair) return dispatch_epi<256, true, false>(a, maps, p, s, tmae);
+      if (mc) return dispatch_epi<256, false, true>(a, maps, p, s, tmae);
+      return dispatch_epi<256, false, false>(a, maps, p, s, tmae);
   }
   return ARMT_ERR_UNSUPPORTED;
 }
 
 int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
   ARMT_REQUIRE(a.K % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs K %% 8 == 0 (K=%d)", a.K);
+  ARMT_REQUIRE(a.a_kwrap >= 0 && a.b_kwrap >= 0 && a.a_kwrap % 64 == 0 && a.b_kwrap % 64 == 0 &&
+               a.a_kwrap < a.K && a.b_kwrap < a.K, ARMT_ERR_DIM, "K wrap must be a multiple of 64 below K");
   ARMT_REQUIRE(a.lda % 8 == 0 && a.ldb % 8 == 0, ARMT_ERR_DIM, "bf16 GEMM needs lda/ldb %% 8 == 0");
   if (a.epilogue == ARMT_EPI_SWIGLU)
     ARMT_REQUIRE((a.swiglu_block == 32 || a.swiglu_block == 128) && a.N % (2 * a.swiglu_block) == 0,
                  ARMT_ERR_UNSUPPORTED, "SwiGLU block must be 32 or 128 and divide N/2");
+  if (a.epilogue == ARMT_EPI_FOLDR)
+    ARMT_REQUIRE(a.N <= 128 && a.c2_split >= a.N && a.c2_split % 16 == 0 && a.ldc >= 4LL * a.c2_split &&
+                 a.ldc % 8 == 0 && a.c_dtype == ARMT_BF16 && a.R != nullptr, ARMT_ERR_UNSUPPORTED,
+                 "FOLDR epilogue: N <= 128 tokens, segment %% 16, ldc >= 4 segments, bf16 C, value rows R");
   if (a.epilogue == ARMT_EPI_DPFP)
     ARMT_REQUIRE((a.N == 16 || a.N == 32 || a.N == 64) && a.nu >= 1 && a.nu <= 3 && a.z != nullptr &&
                  a.den != nullptr && a.ldc >= 2LL * a.nu * a.N && a.ldc % 8 == 0 && a.c_dtype == ARMT_BF16,

@@ -13,10 +13,11 @@ HBM layout
             (L, d, F), wqa (L, d_mem, d), wkvb (L, Nkvb, d) = [W_v; W_k; W_beta; 0],
             unemb (V, d). F = d_ff padded to a multiple of 32 (zero rows/cols).
   state     A (L, d, d_phi) f32, z (L, d_phi) f32 — the reference MemoryState
-            shapes — plus (bf16 mode) the memory operand ``memop`` (L, NB, 3P):
-            per layer the [hi|lo|hi] bf16x3 split of A (rows 0..d-1), of z (row
-            d) and of the current member's phi (rows d+8..), the B operand of the
-            tensor-core fold; retrieval reads its hi part. Refreshed by the fold.
+            shapes — plus (bf16 mode) the memory operand ``memop`` (L, NB, 2P),
+            P = d_phi rounded up to 32: per layer the [hi|lo] bf16 split of A
+            (rows 0..d-1) and of z (row d); the tensor-core fold reads it as a
+            bf16x3 operand (hi re-read as the third part through a K wrap),
+            retrieval reads its hi part. Refreshed by the fold.
   slots     residual stream per in-flight segment: xs (n_slots, T, d) f32 and,
             in bf16 mode, its bf16 copy xs_bf written by the same epilogues.
   members   per-step temporaries stacked over members: h, qkv, ctx, gu, q, phi,
@@ -136,7 +137,7 @@ def prepare_weights(weights: GroupedWeights, dtype_name: str = "bf16", device=No
     dh = cfg.d_head
     T = cfg.tokens_per_segment
     d_phi = cfg.d_phi
-    d_phi_pad = _round_up(d_phi, 8) if bf16 else d_phi
+    d_phi_pad = _round_up(d_phi, 32) if bf16 else d_phi   # [hi | lo] memory operand wraps at 2P (64-col K blocks)
     d_ff_pad = _round_up(dff, 32)
     block = 128 if d_ff_pad % 128 == 0 else 32
     n_kvb = _round_up(d + dm + 1, 16)
@@ -274,8 +275,8 @@ class MemoryState:
         L, d, dphi = self.A.shape
         P = prepared.d_phi_pad
         nb = int(_lib.load().armt_memop_rows(d, prepared.config.num_mem_tokens))
-        if self.memop is None or tuple(self.memop.shape) != (L, nb, 3 * P):
-            self.memop = torch.zeros(L, nb, 3 * P, dtype=torch.bfloat16, device=self.A.device)
+        if self.memop is None or tuple(self.memop.shape) != (L, nb, 2 * P):
+            self.memop = torch.zeros(L, nb, 2 * P, dtype=torch.bfloat16, device=self.A.device)
 
         def split(x):
             hi = x.to(torch.bfloat16)
@@ -284,7 +285,6 @@ class MemoryState:
             hi, lo = split(src)
             self.memop[:, rows, 0:dphi] = hi
             self.memop[:, rows, P:P + dphi] = lo
-            self.memop[:, rows, 2 * P:2 * P + dphi] = hi
 
 
 # ============================================================================
@@ -430,7 +430,7 @@ class Engine:
                                          self.phi.data_ptr(), p.ab, p.d_phi_pad, T * p.d_phi_pad,
                                          self.den.data_ptr(), T, T, cfg.d_mem, cfg.dpfp_nu, stream), "dpfp_den")
         bmat = state.memop if self.bf16 else state.A
-        ld_b = 3 * p.d_phi_pad if self.bf16 else p.d_phi
+        ld_b = 2 * p.d_phi_pad if self.bf16 else p.d_phi
         nb_rows = state.memop.shape[1] if self.bf16 else d
 
         def fill_n(a):

@@ -65,9 +65,14 @@ def main():
     ap.add_argument("--layers", type=int, default=16)
     ap.add_argument("--eps", type=float, default=100.0)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--config", default="c2", choices=["c2", "c1", "mid"])
     args = ap.parse_args()
-    cfg = ModelConfig(n_layers=args.layers, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024,
-                      num_mem_tokens=128, d_mem=64, vocab_size=4096, eps_assoc=args.eps, seed=0)
+    if args.config == "c2":
+        cfg = ModelConfig(n_layers=args.layers, d_model=2048, n_heads=32, d_ff=8192, segment_size=1024,
+                          num_mem_tokens=128, d_mem=64, vocab_size=4096, eps_assoc=args.eps, seed=0)
+    else:
+        from conftest import C1, MID
+        cfg = ModelConfig(**(C1 if args.config == "c1" else MID), eps_assoc=args.eps)
     w = conditioned_weights(cfg)
     S = args.segments
     tokens = cli_tokens(cfg, S * cfg.segment_size - 13, seed=2)
@@ -83,7 +88,7 @@ def main():
     worst = 0.0
     for step in plan.steps:
         for s, slot in step.enters:
-            e.embed(ids[s * 1024:(s + 1) * 1024], slot, stream)
+            e.embed(ids[s * cfg.segment_size:(s + 1) * cfg.segment_size], slot, stream)
         e.retrieve(step.slots, step.layers, st, stream)
         e.forward(step.slots, step.layers, stream)
         e.project_kvb(step.slots, step.layers, stream)

@@ -202,7 +202,7 @@ def main():
             nk = 2128
             kvb = torch.randn(G, M, nk, device="cuda")
             nb = LIB.armt_memop_rows(d, M)
-            memop = torch.zeros(L, nb, 3 * P, device="cuda", dtype=torch.bfloat16)
+            memop = torch.zeros(L, nb, 2 * P, device="cuda", dtype=torch.bfloat16)
             ws = torch.zeros(LIB.armt_fold_tc_workspace_bytes(G, M, d, dphi) // 4 + 1, device="cuda")
             mem = _lib.members(list(range(G)), list(range(G)))
             s = torch.cuda.current_stream().cuda_stream

@@ -32,8 +32,8 @@ tokens = cli_tokens(cfg, S * cfg.segment_size - 5)
 for dtype in ("bf16", "f32"):
     prep = prepare_weights(w, dtype, device="cuda:0")
     st = MemoryState.fresh(cfg, "cuda:0")
-    a, _ = run_diagonal(prep, cfg, tokens, state=st, graph=False)
-    b, _ = run_sequential(prep, cfg, tokens, graph=False)
+    a, _ = run_diagonal(prep, cfg, tokens, dtype=dtype, state=st, graph=False)
+    b, _ = run_sequential(prep, cfg, tokens, dtype=dtype, graph=False)
     assert np.array_equal(a, b), f"{name} {dtype}: schedules disagree"
     assert np.isfinite(a).all()
     print(f"{name} {dtype}: ok", flush=True)

@@ -280,8 +280,8 @@ def _fold64(A0, z0, kvb_g, d, d_mem, nu, eps):
                                               (256, 16, 16, 3, 10.0), (384, 24, 32, 2, 10.0),
                                               (128, 16, 16, 3, 1e-6)])
 def test_tensor_core_fold_matches_in_order_f64(d, M, d_mem, nu, eps):
-    """armt_mem_fold_tc (chunked form: bf16x3 tensor-core GEMMs + blocked
-    triangular solve) against the in-order f64 delta rule on a LIVE state
+    """armt_mem_fold_tc (chunked form: bf16x3 tensor-core GEMMs around the chain
+    and an explicit L^{-1}) against the in-order f64 delta rule on a LIVE state
     (nonzero A, z): A and z within 1e-5 relative, untouched layers bitwise,
     and the bf16x3 memory operand it refreshes equal to a fresh split of the
     new A and z (the retrieval reads it)."""
@@ -289,7 +289,7 @@ def test_tensor_core_fold_matches_in_order_f64(d, M, d_mem, nu, eps):
     from paper_2506_05229_b200.engine import MemoryState
     rng = np.random.default_rng(11)
     dphi = 2 * nu * d_mem
-    P = (dphi + 7) // 8 * 8
+    P = (dphi + 31) // 32 * 32
     G, L = 3, 4
     layers = [3, 0, 2]
     A0 = (rng.standard_normal((L, d, dphi)) * 0.05).astype(np.float32)
@@ -314,12 +314,13 @@ def test_tensor_core_fold_matches_in_order_f64(d, M, d_mem, nu, eps):
         assert rel(st.A[l].cpu(), torch.tensor(Ar)) < 1e-5, (l, rel(st.A[l].cpu(), torch.tensor(Ar)))
         assert rel(st.z[l].cpu(), torch.tensor(zr)) < 1e-5
     assert torch.equal(st.A[1].cpu(), torch.tensor(A0[1]))
-    # the refreshed operand: rows 0..d-1 = [hi | lo | hi] of A, row d = that of z
+    # the refreshed operand: rows 0..d-1 = [hi | lo] of A, row d = that of z
     op = st.memop.float()
+    assert st.memop.shape[2] == 2 * P
     for l in layers:
         hi, lo = op[l, :d, :dphi], op[l, :d, P:P + dphi]
         assert rel(hi + lo, st.A[l]) < 2e-5
-        assert torch.equal(op[l, :d, 2 * P:2 * P + dphi], op[l, :d, :dphi])
+        assert torch.equal(hi, st.A[l].to(torch.bfloat16).float())
         assert rel(op[l, d, :dphi] + op[l, d, P:P + dphi], st.z[l]) < 2e-5
 
 
@@ -485,3 +486,91 @@ def test_tc_gemm_concurrent_remainder_from_many_streams(monkeypatch):
     torch.cuda.synchronize()
     for C in outs[1:]:
         assert torch.equal(C, outs[0])
+
+
+@pytest.mark.parametrize("epi,M,N,K,split,bn", [
+    ("residual", 1152, 2048, 2048, False, None),   # O-projection shape (pair tiles + remainder)
+    ("retrieve", 1152, 2048, 384, False, None),    # retrieval numerator shape
+    ("residual", 2048, 384, 768, True, "128"),     # fold update: A += ..., memop [hi | lo] rows
+    ("residual", 300, 520, 256, False, "64"),      # ragged rows / columns
+    ("retrieve", 77, 1000, 96, False, "256"),
+])
+def test_tc_gemm_tma_epilogue_matches_register_epilogue(epi, M, N, K, split, bn, monkeypatch):
+    """The TMA epilogue of the short-K residual / retrieve GEMMs (residual tile
+    TMA-loaded into swizzled smem, f32 result and bf16 copy TMA-stored) is
+    bitwise the register (coalesced-transpose) epilogue: outputs, bf16 copy or
+    [hi | lo] split, and the per-64-column row sums of squares."""
+    torch.manual_seed(12)
+    G = 3
+    A = torch.randn(G, M, K, device=DEV).bfloat16()
+    B = (torch.randn(G, N, K, device=DEV) * 0.05).bfloat16()
+    X0 = torch.randn(G + 1, M, N, device=DEV)
+    den = torch.randn(G, M, device=DEV)
+    den[:, :7] = 0.25
+    if bn:
+        monkeypatch.setenv("ARMT_GEMM_BN", bn)
+    np_ = -(-N // 64)
+    P = -(-N // 32) * 32
+    slots = [2, 0, 3]
+
+    def run(tmae):
+        monkeypatch.setenv("ARMT_GEMM_TMAE", tmae)
+        X = X0.clone()
+        ssq = torch.zeros(G, M, np_, device=DEV)
+        ld2 = 2 * P if split else N
+        C2 = torch.zeros(G + 1, M, ld2, device=DEV, dtype=torch.bfloat16)
+        kw = dict(epilogue=_lib.EPI_RESIDUAL if epi == "residual" else _lib.EPI_RETRIEVE, R=X.data_ptr(), ldr=N,
+                  r_stride=M * N, C2=C2.data_ptr(), ldc2=ld2, c2_stride=M * ld2, ssq_out=ssq.data_ptr(),
+                  ssq_stride=M * np_, ssq_np=np_)
+        if split:
+            kw["c2_split"] = P
+        if epi == "retrieve":
+            kw.update(den=den.data_ptr(), den_stride=M, eps=0.25)
+        args = gemm_args(G, M, N, K, A, B, X, BF16, F32, c_slots=slots, **kw)
+        _lib.check(LIB.armt_gemm(args, stream()), "gemm")
+        torch.cuda.synchronize()
+        return X, C2, ssq
+
+    ref = run("0")
+    got = run("1")
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+    acc = torch.einsum("gmk,gnk->gmn", A.float(), B.float())
+    if epi == "retrieve":
+        acc = torch.where(den.abs()[..., None] <= 0.25, torch.zeros_like(acc), acc / den[..., None])
+    for g, sl in enumerate(slots):
+        assert rel(got[0][sl], X0[sl] + acc[g]) < 1e-5
+
+
+def test_tc_gemm_k_wrap_reuses_operand_columns():
+    """a_kwrap / b_kwrap: a bf16x3 operand stored as [hi | lo] and read as
+    [hi | lo | hi] through the K wrap gives bitwise the GEMM on the explicit
+    three-part operand (the memory operand and the fold's [V | P] operand)."""
+    torch.manual_seed(13)
+    G, M, N, P = 2, 256, 192, 128
+    hiA = torch.randn(G, M, P, device=DEV).bfloat16()
+    loA = (torch.randn(G, M, P, device=DEV) * 1e-3).bfloat16()
+    Bm = torch.randn(G, N, 3 * P, device=DEV).bfloat16()
+    full = torch.cat([hiA, loA, hiA], -1).contiguous()
+    two = torch.cat([hiA, loA], -1).contiguous()
+    C1 = torch.zeros(G, M, N, device=DEV)
+    C2 = torch.zeros(G, M, N, device=DEV)
+    _lib.check(LIB.armt_gemm(gemm_args(G, M, N, 3 * P, full, Bm, C1, BF16, F32), stream()), "gemm")
+    a = gemm_args(G, M, N, 3 * P, two, Bm, C2, BF16, F32)
+    a.lda, a.a_stride, a.a_kwrap = 2 * P, M * 2 * P, 2 * P
+    _lib.check(LIB.armt_gemm(a, stream()), "gemm")
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)
+    # the same on the B side
+    C3 = torch.zeros(G, M, N, device=DEV)
+    At = torch.randn(G, M, 3 * P, device=DEV).bfloat16()
+    hiB = torch.randn(G, N, P, device=DEV).bfloat16()
+    loB = (torch.randn(G, N, P, device=DEV) * 1e-3).bfloat16()
+    fullB = torch.cat([hiB, loB, hiB], -1).contiguous()
+    twoB = torch.cat([hiB, loB], -1).contiguous()
+    _lib.check(LIB.armt_gemm(gemm_args(G, M, N, 3 * P, At, fullB, C1, BF16, F32), stream()), "gemm")
+    b = gemm_args(G, M, N, 3 * P, At, twoB, C3, BF16, F32)
+    b.ldb, b.b_stride, b.b_kwrap = 2 * P, N * 2 * P, 2 * P
+    _lib.check(LIB.armt_gemm(b, stream()), "gemm")
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C3)
