@@ -192,12 +192,16 @@ def test_attention_matches_reference(dtype, T, H, dh):
 
 @pytest.mark.parametrize("T", [64, 256, 300, 1152])
 @pytest.mark.parametrize("amp", [1.0, 6.0])
-def test_attention_dh64_pairs_and_lazy_rescale(T, amp):
+@pytest.mark.parametrize("G,H", [(3, 2), (1, 3), (4, 32)])
+def test_attention_dh64_pairs_and_lazy_rescale(T, amp, G, H):
     # d_head 64 runs the ping-pong kernel: odd / even / single query-tile counts,
     # a ragged tail, and large scores (amp 6 -> score spread ~ 36 / 8 per row)
-    # that force the lazy running-max raises and O rescales in TMEM
+    # that force the lazy running-max raises and O rescales in TMEM. An odd
+    # member*head count leaves one cross-head tail item with a single group;
+    # (4, 32) gives every CTA several items (the MMA issue and the O epilogue
+    # are pipelined across item boundaries)
     torch.manual_seed(7)
-    G, H, dh = 3, 2, 64
+    dh = 64
     d = H * dh
     qkv = (amp * torch.randn(G, T, 3 * d, device=DEV)).to(torch.bfloat16)
     ctx = torch.zeros(G, T, d, device=DEV, dtype=torch.bfloat16)
