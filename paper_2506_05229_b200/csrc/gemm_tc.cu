@@ -1242,14 +1242,16 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
   p.z = a.z; p.nu = a.nu;
   p.a_kwrap = a.a_kwrap; p.b_kwrap = a.b_kwrap;
   // TMA epilogue for the short-K (epilogue-bound) residual / retrieve GEMMs: residual tiles
-  // TMA-loaded ahead of the accumulator, results TMA-stored (ARMT_GEMM_TMAE=0 disables)
+  // TMA-loaded ahead of the accumulator, results TMA-stored (ARMT_GEMM_TMAE=0 disables).
+  // K <= 1024 only: it costs mainloop stages, so the K=2048 O-projection is faster without
+  // it (C2, G=16: 164 vs 205 us) while the K=384 retrieval gains (86 vs 116 us)
   bool tmae = false;
   {
     const char* te = getenv("ARMT_GEMM_TMAE");
     const bool tmae_on = !(te && te[0] == '0');
     const bool heavy = a.epilogue == ARMT_EPI_RESIDUAL || a.epilogue == ARMT_EPI_RETRIEVE;
     const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-    tmae = tmae_on && heavy && p.xpose && a.K <= 2048 && a.c_dtype == ARMT_F32 && al16(a.C) && al16(a.R) &&
+    tmae = tmae_on && heavy && p.xpose && a.K <= 1024 && a.c_dtype == ARMT_F32 && al16(a.C) && al16(a.R) &&
            a.ldc % 4 == 0 && a.ldr % 4 == 0 && a.c_stride % 4 == 0 && a.r_stride % 4 == 0 &&
            (a.C2 == nullptr || (al16(a.C2) && a.ldc2 % 8 == 0 && a.c2_stride % 8 == 0 && a.c2_split % 32 == 0));
     if (tmae) {

@@ -19,7 +19,7 @@ timeout 600 $NCU --set full --import-source on -k regex:attn -s 3 -c 1 -o gpurun
 timeout 600 $NCU --set full --import-source on -k "regex:fold|gemm" -s 5 -c 5 -o gpurun_out/full_fold \
   python scripts/kernel_bench.py --G 16 --ops foldtc --iters 1 > gpurun_out/full_fold.log 2>&1
 # summarise on the box (ncu -i), keep the summaries + the launch list, drop the big reports
-python scripts/profile_summary.py --tag r1 --out gpurun_out/profiles_new --launches gpurun_out/launches.csv \
+python scripts/profile_summary.py --tag ${TAG:-r2} --out gpurun_out/profiles_new --launches gpurun_out/launches.csv \
   --note "Launch list: \`ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 python bench.py --steps 1 --warmup 0 --segments 24 --no-cpu-baseline\` (C2 width, 24 segments; eager warm pass + one graph replay; cold-cache, serialised launches - compare SHARES, not absolutes). Full captures: \`ncu --set full --import-source on --clock-control none\` of scripts/kernel_bench.py at C2 shapes, G=16 (one wavefront step) unless noted. Command script: scripts/gpu_profile.sh." \
   --full gemm_gu=gpurun_out/full_gu.ncu-rep --full gemm_gu_g8=gpurun_out/full_gu_g8.ncu-rep \
   --full gemm_down=gpurun_out/full_down.ncu-rep --full gemm_qkv_rope=gpurun_out/full_qkv.ncu-rep \

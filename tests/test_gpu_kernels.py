@@ -493,7 +493,7 @@ def test_tc_gemm_concurrent_remainder_from_many_streams(monkeypatch):
 
 
 @pytest.mark.parametrize("epi,M,N,K,split,bn", [
-    ("residual", 1152, 2048, 2048, False, None),   # O-projection shape (pair tiles + remainder)
+    ("residual", 1152, 2048, 1024, False, None),   # pair tiles + remainder (TMA epilogue needs K <= 1024)
     ("retrieve", 1152, 2048, 384, False, None),    # retrieval numerator shape
     ("residual", 2048, 384, 768, True, "128"),     # fold update: A += ..., memop [hi | lo] rows
     ("residual", 300, 520, 256, False, "64"),      # ragged rows / columns
