@@ -100,6 +100,25 @@ __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2; exp2(-inf) =
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// packed f32x2 arithmetic (round-to-nearest, the scalar ops' rounding)
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ float fast_rcp(float x) {  // MUFU.RCP
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -460,8 +479,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         mbar_wait_sleep(&tfull[acc], acc_phase);
         atomicAdd(&g_gemm_prof[5], (unsigned long long)(clock64() - t0));
       }
+      // one warp of the warpgroup polls the accumulator barrier; the other three wait on a
+      // named barrier (blocked in hardware, no issue slots or power spent re-polling)
       __syncwarp();
-      mbar_wait_sleep(&tfull[acc], acc_phase);
+      if (ew == 0) mbar_wait_sleep(&tfull[acc], acc_phase);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + eg) : "memory");
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       const long long off = (long long)c_slot * p.c_stride + (long long)row * p.ldc;
@@ -615,17 +637,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           __syncwarp();
           tmem_ld32(tbase + c0, gte);
           tmem_ld32(tbase + BN / 2 + c0, up);
+#if ARMT_SWIGLU_FAST
+          // silu(g) = g / (1 + 2^(-g log2 e)): MUFU.EX2 + MUFU.RCP (approximate, ~2 ulp, far
+          // below the bf16 rounding of the output) instead of the IEEE reciprocal sequence.
+          // The multiplies and the add run as packed f32x2 pairs (the same IEEE operations in
+          // the same order as the scalar form, so bitwise the same result, in half the issues).
+          const unsigned long long rs2 = pk2(rs, rs), nl2 = pk2(-1.4426950408889634f, -1.4426950408889634f),
+                                   one2 = pk2(1.f, 1.f);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const unsigned long long gv = fmul2(pk2(gte[j], gte[j + 1]), rs2);
+            float e0, e1;
+            upk2(fmul2(nl2, gv), e0, e1);
+            const unsigned long long den = fadd2(one2, pk2(fast_exp2(e0), fast_exp2(e1)));
+            float d0, d1;
+            upk2(den, d0, d1);
+            const unsigned long long a = fmul2(gv, pk2(fast_rcp(d0), fast_rcp(d1)));
+            upk2(fmul2(a, fmul2(pk2(up[j], up[j + 1]), rs2)), gte[j], gte[j + 1]);
+          }
+#else
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float gv = gte[j] * rs;
-#if ARMT_SWIGLU_FAST
-            // silu(g) = g / (1 + 2^(-g log2 e)): MUFU.EX2 + MUFU.RCP (approximate, ~2 ulp, far
-            // below the bf16 rounding of the output) instead of the IEEE reciprocal sequence
-            gte[j] = gv * fast_rcp(1.f + fast_exp2(-1.4426950408889634f * gv)) * (up[j] * rs);
-#else
             gte[j] = gv * __frcp_rn(1.f + __expf(-gv)) * (up[j] * rs);
-#endif
           }
+#endif
           if (p.cst && out_n0 + c0 + 32 <= p.N / 2) {
             store_chunk_bf16_coalesced(reinterpret_cast<uint4*>(xpose) + (warp - 4) * 128, lane, gte,
                                        reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)c_slot * p.c_stride,
