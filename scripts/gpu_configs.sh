@@ -15,7 +15,7 @@ import json, sys
 f = sys.argv[1]
 try:
     d = json.loads([l for l in open(f) if l.startswith("{")][-1])
-    print(f, round(d["value"]), round(d["ms_per_step"], 1), round(d["e2e"]["value"]), d["config"]["whole_step_frac_of_sustained"], d["clocks"]["sm_mhz"])
+    print(f, round(d["value"]), round(d["ms_per_step"], 1), round(d["e2e"]["value"]), d.get("whole_step_frac_of_sustained"), d["clocks"]["sm_mhz"])
 except Exception as e:
     print(f, "FAILED", e)
 PY
