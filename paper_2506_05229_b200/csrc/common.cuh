@@ -37,6 +37,19 @@ std::atomic<long long>& launch_counter();
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int num_sms();
+
+// A forked side stream per calling stream (created on first use, reused by every later
+// call and graph capture from that stream): fork() makes the side stream wait for the
+// caller's work so far, join() makes the caller wait for the side stream's. nullptr when
+// more than 32 calling streams are in use; callers then run their side work in order on
+// their own stream.
+struct ForkedStream {
+  cudaStream_t caller, side;
+  cudaEvent_t fork_ev, join_ev;
+  int fork();
+  int join();
+};
+ForkedStream* forked_stream(cudaStream_t caller);
 bool pdl_enabled();   // programmatic dependent launch for the tensor-core kernels (ARMT_PDL=0: off)
 
 // ---- device helpers -------------------------------------------------------------

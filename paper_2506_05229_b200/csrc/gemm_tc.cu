@@ -1113,8 +1113,7 @@ static int pick_bn(const ArmtGemmArgs& a) {
     const double size = bn == 256 ? 1.0 : bn == 128 ? 0.93 : 0.8;   // per-tile efficiency
     // a single wave leaves every CTA's epilogue exposed (nothing to overlap it with):
     // small grouped GEMMs (memory-token k/v/beta, fold) prefer two tiles per CTA
-    static const bool w1pen = !(getenv("ARMT_GEMM_W1PEN") && getenv("ARMT_GEMM_W1PEN")[0] == '0');
-    const double one_wave = (w1pen && waves == 1 && tiles > sms / 2) ? 0.8 : 1.0;
+    const double one_wave = (waves == 1 && tiles > sms / 2) ? 0.8 : 1.0;
     const double score = fill * useful * size * one_wave;
     if (score > best_score + 1e-9) { best_score = score; best = bn; }
   }
@@ -1247,23 +1246,16 @@ static int gemm_rows(const ArmtGemmArgs& a, int bn, bool pair, int row0, int m_e
     }
     if (dyn_on && ring.load() != nullptr) p.tile_ctr = ring.load() + 2 * (next.fetch_add(1) % RING);
   }
-  if (p.max_ctas == 0) {   // experiments: ARMT_GEMM_MAXCTAS caps every launch
-    static const char* mc = getenv("ARMT_GEMM_MAXCTAS");
-    if (mc) p.max_ctas = atoi(mc);
-  }
   {
     // coalesced residual epilogue needs 16 B-aligned f32 rows and 8 B-aligned bf16 rows
-    const char* xe = getenv("ARMT_GEMM_XPOSE");
     const bool al = (a.N % 4 == 0) && (a.ldc % 4 == 0) && (a.ldr % 4 == 0) &&
                     ((reinterpret_cast<uintptr_t>(a.C) | reinterpret_cast<uintptr_t>(a.R)) % 16 == 0) &&
                     (a.C2 == nullptr || (a.ldc2 % 4 == 0 && a.c2_split % 4 == 0 &&
                                          reinterpret_cast<uintptr_t>(a.C2) % 8 == 0)) &&
                     (a.c_stride % 4 == 0) && (a.r_stride % 4 == 0) && (a.C2 == nullptr || a.c2_stride % 4 == 0);
-    p.xpose = al && !(xe && xe[0] == '0') ? 1 : 0;
-    const char* ce = getenv("ARMT_GEMM_CST");
+    p.xpose = al ? 1 : 0;
     p.cst = (a.c_dtype == ARMT_BF16 || a.epilogue == ARMT_EPI_SWIGLU || a.epilogue == ARMT_EPI_ROPE) &&
-            a.ldc % 8 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 && a.c_stride % 8 == 0 &&
-            !(ce && ce[0] == '0') ? 1 : 0;
+            a.ldc % 8 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 && a.c_stride % 8 == 0 ? 1 : 0;
   }
   {
     static const bool prof = getenv("ARMT_GEMM_PROF") != nullptr;
@@ -1329,34 +1321,23 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
                  a.den != nullptr && a.ldc >= 2LL * a.nu * a.N && a.ldc % 8 == 0 && a.c_dtype == ARMT_BF16,
                  ARMT_ERR_UNSUPPORTED, "DPFP epilogue: d_mem in {16,32,64}, nu in [1,3], bf16 phi, ldc %% 8");
   const int bn = tc::pick_bn(a);
-  // CTA-pair (cta_group::2, 256-row tiles) for mainloop-bound 256-wide GEMMs: rows
-  // [0, 256*floor(M/256)) as pair tiles, the remainder as single-CTA tiles (no padded
-  // MMA work). Epilogue-bound shapes (short-K residual/retrieve) stay single-CTA.
-  // ARMT_GEMM_PAIR=0 disables pairs (A/B runs).
+  // Engine policy for 256-wide tiles (measured in situ, C2):
+  //   * M a whole number of 256-row pairs (LM head)            -> CTA pairs (cta_group::2)
+  //   * QKV+RoPE and the residual GEMMs (O, down) of 1152-row members -> pair tiles for rows
+  //     [0, 1024) of every member CONCURRENT with single-CTA tiles for the remainder rows on
+  //     a forked stream with REM_CTAS SMs (down -9%, QKV -6%, O -0.5% vs the alternatives)
+  //   * other mainloop-heavy shapes with an even number of N tiles (gate/up) -> 2-CTA
+  //     multicast clusters sharing the weight tile (pairs measured slower there)
+  //   * everything else -> single-CTA tiles
+  // ARMT_GEMM_PAIR=0 / =split / =conc and ARMT_GEMM_MC=0 override it (tests, A/B runs).
   const char* pe = getenv("ARMT_GEMM_PAIR");
-  const bool heavy_epi = a.epilogue == ARMT_EPI_RESIDUAL || a.epilogue == ARMT_EPI_RETRIEVE;
   const int m_pair = (a.M / (2 * tc::BM)) * (2 * tc::BM);
-  // Pairs where M fills whole pair tiles. ARMT_GEMM_PAIR=split also splits 1152-row members
-  // into 4 pair tiles + a single-CTA remainder launch after it (base clocks: down -3%, qkv
-  // -1.5%, gate/up +7% slower); ARMT_GEMM_PAIR=conc runs that remainder CONCURRENTLY on a
-  // forked stream with ARMT_GEMM_REM_CTAS SMs (default 20) while the pair tiles use the rest.
-  // Default policy (in-situ step breakdown, same box): whole-pair shapes -> pairs (LM head
-  // -11%); the QKV+RoPE GEMM and the K=8192 down-projection -> concurrent remainder (-6%,
-  // -9%); gate/up stays a multicast cluster (pairs measured slower there).
   const bool split = pe && strcmp(pe, "split") == 0;
-  // the long-K residual GEMM (down-projection) also runs pair tiles + concurrent remainder:
-  // -9% on the op in situ, -1.4% per forward (ARMT_GEMM_CONC_DOWN=0 disables)
-  static const bool conc_down = !(getenv("ARMT_GEMM_CONC_DOWN") && getenv("ARMT_GEMM_CONC_DOWN")[0] == '0');
-  // ... and so does the O-projection residual GEMM (-0.5% per forward; ARMT_GEMM_CONC_O=0 disables)
-  static const bool conc_o = !(getenv("ARMT_GEMM_CONC_O") && getenv("ARMT_GEMM_CONC_O")[0] == '0');
   const bool conc = (pe && strcmp(pe, "conc") == 0) ||
-                    (!pe && (a.epilogue == ARMT_EPI_ROPE || (conc_down && a.epilogue == ARMT_EPI_RESIDUAL && a.K >= 4096) ||
-                             (conc_o && a.epilogue == ARMT_EPI_RESIDUAL)));
-  const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) &&
-                    a.K >= (heavy_epi && !conc_o ? 4096 : 1024) && !(pe && pe[0] == '0');
+                    (!pe && (a.epilogue == ARMT_EPI_ROPE || a.epilogue == ARMT_EPI_RESIDUAL));
+  const bool pair = bn == 256 && m_pair > 0 && (m_pair == a.M || split || conc) && a.K >= 1024 &&
+                    !(pe && pe[0] == '0');
   if (!pair) {
-    // multicast clusters (ARMT_GEMM_MC=0 disables): 256-wide tiles, an even number of
-    // n-blocks (pair slots), mainloop-heavy shapes
     const char* me = getenv("ARMT_GEMM_MC");
     const int tiles_n = (a.N + bn - 1) / bn;
     const bool mc = bn == 256 && (tiles_n % 2 == 0) && a.K >= 1024 && !(me && me[0] == '0') && a.max_ctas == 0;
@@ -1367,43 +1348,51 @@ int gemm_tc(const ArmtGemmArgs& a, cudaStream_t s) {
     int rc = gemm_rows(a, bn, true, 0, m_pair, s);
     return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
   }
-  // one forked stream per calling stream (callers on different streams stay independent)
-  struct Fork { cudaStream_t caller, side; cudaEvent_t fork_ev, join_ev; };
-  constexpr int MAX_FORKS = 32;
-  static Fork forks[MAX_FORKS];
-  static int n_forks = 0;
-  static std::mutex fork_mu;
-  Fork* fk = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(fork_mu);
-    for (int i = 0; i < n_forks; ++i)
-      if (forks[i].caller == s) fk = &forks[i];
-    if (fk == nullptr && n_forks == MAX_FORKS) {
-      // more calling streams than fork slots: run the remainder after the pair tiles
-      int rc = gemm_rows(a, bn, true, 0, m_pair, s);
-      return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
-    }
-    if (fk == nullptr) {
-      fk = &forks[n_forks++];
-      fk->caller = s;
-      cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&fk->fork_ev, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&fk->join_ev, cudaEventDisableTiming);
-    }
+  ForkedStream* fk = forked_stream(s);
+  if (fk == nullptr) {   // more calling streams than fork slots: the remainder after the pair tiles
+    int rc = gemm_rows(a, bn, true, 0, m_pair, s);
+    return rc ? rc : gemm_rows(a, bn, false, m_pair, a.M, s);
   }
-  cudaStream_t side = fk->side;
-  cudaEvent_t fork_ev = fk->fork_ev, join_ev = fk->join_ev;
   const char* rc_env = getenv("ARMT_GEMM_REM_CTAS");
   const int rem = rc_env ? atoi(rc_env) : 20;
   const int sms = num_sms();
-  ARMT_REQUIRE(cudaEventRecord(fork_ev, s) == cudaSuccess, ARMT_ERR_CUDA, "gemm fork record");
-  ARMT_REQUIRE(cudaStreamWaitEvent(side, fork_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "gemm fork wait");
-  int rc = gemm_rows(a, bn, false, m_pair, a.M, side, rem);
+  int rc = fk->fork();
+  if (rc) return rc;
+  rc = gemm_rows(a, bn, false, m_pair, a.M, fk->side, rem);
   if (rc) return rc;
   rc = gemm_rows(a, bn, true, 0, m_pair, s, ((sms - rem) / 2) * 2);
   if (rc) return rc;
-  ARMT_REQUIRE(cudaEventRecord(join_ev, side) == cudaSuccess, ARMT_ERR_CUDA, "gemm join record");
-  ARMT_REQUIRE(cudaStreamWaitEvent(s, join_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "gemm join wait");
+  return fk->join();
+}
+
+ForkedStream* forked_stream(cudaStream_t caller) {
+  constexpr int MAX_FORKS = 32;
+  static ForkedStream forks[MAX_FORKS];
+  static int n_forks = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < n_forks; ++i)
+    if (forks[i].caller == caller) return &forks[i];
+  if (n_forks == MAX_FORKS) return nullptr;
+  ForkedStream* f = &forks[n_forks];
+  f->caller = caller;
+  if (cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&f->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&f->join_ev, cudaEventDisableTiming) != cudaSuccess)
+    return nullptr;
+  ++n_forks;
+  return f;
+}
+
+int ForkedStream::fork() {
+  ARMT_REQUIRE(cudaEventRecord(fork_ev, caller) == cudaSuccess, ARMT_ERR_CUDA, "fork: event record");
+  ARMT_REQUIRE(cudaStreamWaitEvent(side, fork_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "fork: stream wait");
+  return ARMT_OK;
+}
+
+int ForkedStream::join() {
+  ARMT_REQUIRE(cudaEventRecord(join_ev, side) == cudaSuccess, ARMT_ERR_CUDA, "join: event record");
+  ARMT_REQUIRE(cudaStreamWaitEvent(caller, join_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "join: stream wait");
   return ARMT_OK;
 }
 

@@ -785,28 +785,11 @@ int fold_v2(const ArmtMembers* mem, const float* kvb, long long ld_kvb, long lon
   ARMT_CHECK_LAUNCH("fold_prep");
 
   // GEMM-R on a forked stream: [V^T | P^T] needs only phi, so it overlaps the chain
-  struct Fork { cudaStream_t caller, side; cudaEvent_t fork_ev, join_ev; };
-  constexpr int MAX_FORKS = 32;
-  static Fork forks[MAX_FORKS];
-  static int n_forks = 0;
-  static std::mutex mu;
-  Fork* fk = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    for (int i = 0; i < n_forks; ++i)
-      if (forks[i].caller == s) fk = &forks[i];
-    if (fk == nullptr && n_forks < MAX_FORKS) {
-      fk = &forks[n_forks++];
-      fk->caller = s;
-      cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&fk->fork_ev, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&fk->join_ev, cudaEventDisableTiming);
-    }
-  }
+  ForkedStream* fk = forked_stream(s);
   cudaStream_t sr = s;
   if (fk != nullptr) {
-    ARMT_REQUIRE(cudaEventRecord(fk->fork_ev, s) == cudaSuccess, ARMT_ERR_CUDA, "fold fork record");
-    ARMT_REQUIRE(cudaStreamWaitEvent(fk->side, fk->fork_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "fold fork wait");
+    const int rc = fk->fork();
+    if (rc) return rc;
     sr = fk->side;
   }
   {
@@ -829,8 +812,8 @@ int fold_v2(const ArmtMembers* mem, const float* kvb, long long ld_kvb, long lon
   fold_w_kernel<<<dim3((q.dphi + 31) / 32, G), 256, w_smem, s>>>(*mem, eps, z, mo, q, w);
   ARMT_CHECK_LAUNCH("fold_w");
   if (fk != nullptr) {
-    ARMT_REQUIRE(cudaEventRecord(fk->join_ev, sr) == cudaSuccess, ARMT_ERR_CUDA, "fold join record");
-    ARMT_REQUIRE(cudaStreamWaitEvent(s, fk->join_ev, 0) == cudaSuccess, ARMT_ERR_CUDA, "fold join wait");
+    const int rc = fk->join();
+    if (rc) return rc;
   }
   // GEMM3: A[layer] += [V^T | P^T] [Y ; Z]^T (K = 6 Mp over a 4 Mp operand); memop rows [0, d) <- split(A)
   ArmtGemmArgs a;
