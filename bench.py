@@ -344,7 +344,7 @@ def reference_arm(args, rank, world):
 def shared_config(args, cfg, n, S, desc) -> dict:
     """The workload identity both arms report (identical dicts for the same flags)."""
     return {"workload": f"{desc}, {n} tokens", "schedule": args.schedule, "segments": S,
-            "init": args.init or ("device" if args.config == "c5" else "reference"),
+            "init": args.init or "reference",
             "eps_assoc": cfg.eps_assoc, "output": "fused NLL (no logits)" if (args.scoring or args.config == "c4")
             else "logits", "l2": "inputs > L2 (3.3 GB bf16 weights, 33.6 GB logits); no flush"}
 
@@ -367,7 +367,7 @@ def device_arm(args, rank, world):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     t_setup = time.time()
-    init = args.init or ("device" if args.config == "c5" else "reference")
+    init = args.init or "reference"
     scoring_value = args.scoring or args.config == "c4"
     w = make_weights(cfg, init)
     tokens = np.random.default_rng([0, n]).integers(0, cfg.vocab_size, n, dtype=np.int64)
