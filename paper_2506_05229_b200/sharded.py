@@ -265,6 +265,8 @@ class DeviceBackend:
         if self.mode == "eager":
             fn()
         elif self.mode == "capture":
+            if key in self.graphs:
+                return   # same launch sequence as an earlier step (same slots / layers): one graph serves both
             g = torch.cuda.CUDAGraph()
             if getattr(self, "_cap_stream", None) is None:
                 self._cap_stream = torch.cuda.Stream()   # one capture stream for every step graph

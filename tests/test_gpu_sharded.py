@@ -98,6 +98,41 @@ def test_sharded_session_single_rank_matches_session():
     assert torch.allclose(got_nll, want_nll, rtol=1e-5, atol=1e-5)
 
 
+def test_sharded_capture_keeps_one_graph_per_launch_sequence():
+    """Steps with the same (slots, layers) repeat as the slots cycle; the capture
+    pass keeps ONE graph per distinct launch sequence and every kept graph is
+    replayed (a re-captured duplicate used to replace the first graph, orphaning
+    anything recorded in it, e.g. the bench's in-graph roofline probe events)."""
+    from paper_2506_05229_b200.sharded import ShardedSession
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    w = conditioned_weights(cfg)
+    n = 12 * cfg.segment_size
+    tokens = torch.as_tensor(cli_tokens(cfg, n, seed=9)).cuda()
+    sh = ShardedSession(w, cfg, n, rank=0, world=1)
+    sh._load_ids(tokens)
+    sh.warm_eager()
+    eager = sh.forward().clone()
+    sh.capture()
+    graphs = sh.backend.graphs
+    step_keys = [k for k in graphs if k[0] == "step"]
+    assert len(step_keys) < sum(1 for st in sh.plan.steps if st.nodes)   # repeats exist at 12 segments
+    used = set()
+
+    class Counting:
+        def __init__(self, key, g):
+            self.key, self.g = key, g
+
+        def replay(self):
+            used.add(self.key)
+            self.g.replay()
+
+    for k in list(graphs):
+        graphs[k] = Counting(k, graphs[k])
+    got = sh.forward()
+    assert torch.equal(got, eager)
+    assert used == set(graphs)
+
+
 @pytest.mark.parametrize("P", [2, 3, 8])
 def test_vocab_parallel_nll_combine_matches_full_vocab(P):
     """Per-rank vocab blocks -> fused LSE partials -> per-row (max, sum) ->
