@@ -431,7 +431,8 @@ constexpr int PS2 = 4;   // phi row padding (floats): rows stay 16-byte aligned 
 __global__ void __launch_bounds__(256) fold_prep_kernel(const __grid_constant__ ArmtMembers mem,
                                                         const float* __restrict__ kvb, long long ld_kvb,
                                                         long long kvb_stride, int k_off, int b_off,
-                                                        const float* __restrict__ z, int d_mem, Geom q, Ws2 w) {
+                                                        const float* __restrict__ z, int d_mem, Geom q, Ws2 w,
+                                                        bool phi_only) {
   extern __shared__ __align__(16) float sm[];
   const int two_m = 2 * d_mem, P = q.P, PS = P + PS2, M = q.M, Mp = q.Mp;
   const int RS = two_m + 1;
@@ -443,7 +444,12 @@ __global__ void __launch_bounds__(256) fold_prep_kernel(const __grid_constant__ 
   int* ta = reinterpret_cast<int*>(sb + TB2);   // [P] first factor index (-1: zero feature)
   int* tb = ta + P;                              // [P] second factor index
   int t = blockIdx.x, bi = 0;
-  while (t > bi) { t -= bi + 1; ++bi; }
+  if (phi_only) {   // grid (nbt, G): the per-token outputs of token block blockIdx.x only
+    bi = t;
+    t = bi;
+  } else {
+    while (t > bi) { t -= bi + 1; ++bi; }
+  }
   const int bj = t;
   const int g = blockIdx.y, layer = mem.layer[g];
   const float* kv = kvb + (long long)g * kvb_stride;
@@ -495,6 +501,7 @@ __global__ void __launch_bounds__(256) fold_prep_kernel(const __grid_constant__ 
     }
   }
   __syncthreads();
+  if (!phi_only) {
   const float* pr = sp;
   const float* pc = sp + (nsrc - 1) * TB2 * PS;
   // K block: thread (ty, tx) -> rows {ty, ty+16} x cols {tx, tx+16}; 4 features per step
@@ -532,6 +539,7 @@ __global__ void __launch_bounds__(256) fold_prep_kernel(const __grid_constant__ 
         if (i == j) w.nrm[(long long)g * Mp + i] = kk;
       }
     }
+  }
   if (bi != bj) return;
   // per-token outputs of the diagonal block: thread = feature
   const int i0 = bi * TB2;
@@ -558,6 +566,93 @@ __global__ void __launch_bounds__(256) fold_prep_kernel(const __grid_constant__ 
     if (lane == 0) {
       w.c[(long long)g * Mp + i] = cz;
       w.beta[(long long)g * Mp + i] = i < M ? sigmoid_ref(sb[tt]) : 0.f;
+    }
+  }
+}
+
+// grid (nbt (nbt + 1) / 2, G), 256 threads, two CTAs per SM: CTA (bi, bj), bi >= bj, computes
+// the fp32 block K[bi][bj] = Phi_bi Phi_bj^T (and its mirror; diagonal blocks also nrm) from
+// the phi rows fold_prep (phi-only mode) wrote — one wave at C2 instead of fold_prep's two.
+// 4 feature quarters x 64 threads, thread (ty, tx) -> rows {ty + 8u} x cols {tx + 8v}, 4
+// features per step (float4 reads, packed f32x2 FMAs), partial blocks summed in a fixed order
+// through shared memory, so K[a][b] and K[b][a] are the identical sum and K is symmetric.
+__global__ void __launch_bounds__(256, 2) fold_k_kernel(Geom q, Ws2 w) {
+  extern __shared__ __align__(16) float sm[];
+  const int P = q.P, PS = P + PS2, M = q.M, Mp = q.Mp, dphi = q.dphi;
+  float* sp = sm;   // [2][TB2][PS]
+  int t = blockIdx.x, bi = 0;
+  while (t > bi) { t -= bi + 1; ++bi; }
+  const int bj = t, g = blockIdx.y, tid = threadIdx.x;
+  const int nsrc = bi == bj ? 1 : 2;
+  const float* ph = w.phi32 + (long long)g * M * dphi;
+  const bool vec = (dphi & 3) == 0;
+  for (int s2 = 0; s2 < nsrc; ++s2) {
+    const int i0 = (s2 == 0 ? bi : bj) * TB2;
+    float* dst = sp + s2 * TB2 * PS;
+    if (vec) {
+      const int c4n = P / 4;
+      for (int e = tid; e < TB2 * c4n; e += 256) {
+        const int tt = e / c4n, c4 = e - tt * c4n;
+        float* d4 = dst + tt * PS + 4 * c4;
+        if (i0 + tt < M && 4 * c4 < dphi) cpa16(d4, ph + (long long)(i0 + tt) * dphi + 4 * c4);
+        else *reinterpret_cast<float4*>(d4) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      for (int e = tid; e < TB2 * P; e += 256) {
+        const int tt = e / P, c = e - tt * P;
+        const bool ok = i0 + tt < M && c < dphi;
+        cpa4(dst + tt * PS + c, ph + (ok ? (long long)(i0 + tt) * dphi + c : 0), ok);
+      }
+    }
+  }
+  cpa_wait_all();
+  __syncthreads();
+  const float* pr = sp;
+  const float* pc = sp + (nsrc - 1) * TB2 * PS;
+  const int qf = tid >> 6, t64 = tid & 63, tx = t64 & 7, ty = t64 >> 3;
+  const int c4_0 = qf * (P / 16), c4_1 = c4_0 + P / 16;   // P is a multiple of 32
+  unsigned long long k2[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) k2[u][v] = 0ull;
+#pragma unroll 2
+  for (int c4 = c4_0; c4 < c4_1; ++c4) {
+    float4 ra[4], rb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ra[u] = reinterpret_cast<const float4*>(pr + (ty + 8 * u) * PS)[c4];
+      rb[u] = reinterpret_cast<const float4*>(pc + (tx + 8 * u) * PS)[c4];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        k2[u][v] = ffma2(f2u(ra[u].x, ra[u].y), f2u(rb[v].x, rb[v].y), k2[u][v]);
+        k2[u][v] = ffma2(f2u(ra[u].z, ra[u].w), f2u(rb[v].z, rb[v].w), k2[u][v]);
+      }
+  }
+  __syncthreads();   // sp is free: every thread is past its reads
+  constexpr int RW = TB2 + 1;
+  float* red = sp;   // [4][TB2][RW]
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float2 kv2 = u2f(k2[u][v]);
+      red[(qf * TB2 + ty + 8 * u) * RW + tx + 8 * v] = kv2.x + kv2.y;
+    }
+  __syncthreads();
+  float* Kg = w.K + (long long)g * Mp * Mp;
+  for (int e = tid; e < TB2 * TB2; e += 256) {
+    const int ii = e / TB2, jj = e - ii * TB2;
+    const float kk = ((red[ii * RW + jj] + red[(TB2 + ii) * RW + jj]) + red[(2 * TB2 + ii) * RW + jj]) +
+                     red[(3 * TB2 + ii) * RW + jj];
+    const int i = bi * TB2 + ii, j = bj * TB2 + jj;
+    if (i < Mp && j < Mp) {
+      Kg[(long long)i * Mp + j] = kk;
+      Kg[(long long)j * Mp + i] = kk;
+      if (i == j) w.nrm[(long long)g * Mp + i] = kk;
     }
   }
 }
@@ -780,9 +875,24 @@ int fold_v2(const ArmtMembers* mem, const float* kvb, long long ld_kvb, long lon
                                             (size_t)2 * TB2 * (2 * d_mem + 1) + 3 * (size_t)q.P + TB2);
   ARMT_REQUIRE(prep_smem <= 227 * 1024, ARMT_ERR_UNSUPPORTED, "fold_tc: d_phi too large");
   cudaFuncSetAttribute(fold_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
-  fold_prep_kernel<<<dim3(nbt * (nbt + 1) / 2, G), 256, prep_smem, s>>>(*mem, kvb, ld_kvb, kvb_stride, k_off,
-                                                                        b_off, z, d_mem, q, w);
-  ARMT_CHECK_LAUNCH("fold_prep");
+  const int kblocks = nbt * (nbt + 1) / 2 * G;
+  if (kblocks <= armt::num_sms()) {
+    // one wave: phi and the K blocks in one kernel (one CTA per SM, 153 KB of phi rows)
+    fold_prep_kernel<<<dim3(nbt * (nbt + 1) / 2, G), 256, prep_smem, s>>>(*mem, kvb, ld_kvb, kvb_stride, k_off,
+                                                                          b_off, z, d_mem, q, w, false);
+    ARMT_CHECK_LAUNCH("fold_prep");
+  } else {
+    // more K blocks than SMs (C2, G = 16: 160): phi, c, beta and the GEMM-R operand per token
+    // block first, then K = Phi Phi^T from those rows at two CTAs per SM — one wave instead of
+    // two (G = 16: 29 vs 35 us; at G = 1 the extra launch would cost 4 us, hence the switch)
+    fold_prep_kernel<<<dim3(nbt, G), 256, prep_smem, s>>>(*mem, kvb, ld_kvb, kvb_stride, k_off, b_off, z, d_mem,
+                                                           q, w, true);
+    ARMT_CHECK_LAUNCH("fold_prep");
+    const size_t k_smem = sizeof(float) * std::max((size_t)2 * TB2 * (q.P + PS2), (size_t)4 * TB2 * (TB2 + 1));
+    cudaFuncSetAttribute(fold_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k_smem);
+    fold_k_kernel<<<dim3(nbt * (nbt + 1) / 2, G), 256, k_smem, s>>>(q, w);
+    ARMT_CHECK_LAUNCH("fold_k");
+  }
 
   // GEMM-R on a forked stream: [V^T | P^T] needs only phi, so it overlaps the chain
   ForkedStream* fk = forked_stream(s);
