@@ -97,7 +97,7 @@ class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, index: int):
         self.index = index
@@ -129,7 +129,7 @@ class ClockSampler:
         return False
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
@@ -143,8 +143,13 @@ class ClockSampler:
             for n, v in zip(names, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
+            try:
+                power.append(float(parts[6]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(power) if power else None}
 
 
 def make_weights(cfg, init: str = "reference"):
@@ -486,12 +491,43 @@ def device_arm(args, rank, world):
     e2e_value = n / (e2e_total / args.steps / 1e3)
     mean_nll = float(host_nll.mean())
 
+    # the reference's own entry point as a drop-in (armt/executors.py:153-226): run_diagonal with
+    # host int64 ids, logits returned on the device (return_numpy=False; the numpy copy of 33.6 GB
+    # of logits would time PCIe, not the forward). Its first call runs eagerly, the second captures
+    # the graph that every later call replays; the clone of the logits is part of each call.
+    d_ff_pad = sess.p.d_ff_pad
+    ref_api = None
+    if world == 1 and not args.force_sharded and args.schedule == "diagonal" and not scoring_value:
+        from paper_2506_05229_b200.executors import clear_caches, run_diagonal
+        del sess
+        sess = None
+        torch.cuda.empty_cache()
+        toks_np = np.asarray(tokens, dtype=np.int64)
+        for _ in range(2):
+            run_diagonal(prep, cfg, toks_np, return_numpy=False)
+        torch.cuda.synchronize()
+        api_ms = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out, _ = run_diagonal(prep, cfg, toks_np, return_numpy=False)
+            e1.record()
+            torch.cuda.synchronize()
+            api_ms.append(e0.elapsed_time(e1))
+            del out
+        ref_api = {"value": n / (statistics.mean(api_ms) / 1e3), "unit": "tokens/s",
+                   "h2d_bytes_per_step": int(n * 8), "d2h_bytes_per_step": 0,
+                   "api": "run_diagonal(prepared, config, host int64 ids, return_numpy=False): the reference's "
+                          "entry point, cached prepared weights, one graph replay + logits clone per call"}
+        clear_caches()
+        torch.cuda.empty_cache()
+
     # north-star ratio in the same run: the sequential segment schedule (armt/executors.py:123-150),
     # same kernels (G = 1 lane), same whole-run CUDA-graph policy, same K/W, fresh memory per replay
     seq_value = None
-    d_ff_pad = sess.p.d_ff_pad
+    seq_clock_summary = None
     if args.compare_sequential and world == 1 and not args.force_sharded and args.schedule == "diagonal":
-        del sess
+        sess = None
         torch.cuda.empty_cache()
         seq = Session(prep, n, schedule="sequential", scoring=scoring_value)
         seq._load_ids(torch.as_tensor(tokens).to(dev))
@@ -500,14 +536,16 @@ def device_arm(args, rank, world):
             seq.forward()
         torch.cuda.synchronize()
         seq_ms = []
-        for _ in range(args.steps):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            seq.forward()
-            e1.record()
-            torch.cuda.synchronize()
-            seq_ms.append(e0.elapsed_time(e1))
+        with ClockSampler(dev.index) as seq_clocks:
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                seq.forward()
+                e1.record()
+                torch.cuda.synchronize()
+                seq_ms.append(e0.elapsed_time(e1))
+        seq_clock_summary = seq_clocks.summary()
         seq_value = n / (statistics.mean(seq_ms) / 1e3)
         del seq
         torch.cuda.empty_cache()
@@ -576,8 +614,10 @@ def device_arm(args, rank, world):
                        if not sharded else "ShardedSession(scoring=True).nll: pinned ids in, per-token NLL out "
                                           "(vocab-parallel fused NLL, all-gathered row partials)",
                 "mean_nll": mean_nll},
+        "e2e_reference_api": ref_api,
         "sequential_value": seq_value,
         "diag_over_seq": (value / seq_value) if seq_value else None,
+        "sequential_clocks": seq_clock_summary,
         "north_star_target": "diagonal >= 1.8x sequential on 1xB200 at C2" if seq_value else None,
         "gpu_launches": int(launches_per_forward * args.steps),
         "clocks": clocks.summary(),
