@@ -271,7 +271,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], PAIR ? 8 : 4); }
     for (int i = 0; i < QD; ++i) { mbar_init(&tq_full[i], 1); mbar_init(&tq_empty[i], 5); }
     if constexpr (TMAE)
-      for (int i = 0; i < 16; ++i) mbar_init(&rbar[i], 1);
+      for (int i = 0; i < 24; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -450,7 +450,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int eg = (warp - 4) >> 2;
     const int acc = eg;
     uint32_t acc_phase = 0;
-    uint32_t rph = 0;   // TMAE: parity of this warp's two residual-tile barriers
+    uint32_t rph = 0;   // TMAE: parity of this warp's residual-tile barriers (one bit per buffer)
     int qk = eg;
     auto first = [&]() { const int t = tile0 + eg * tstep; return t < p.num_tiles ? t : -1; };
     for (int tile = dyn ? tq_pop(qk, true) : first(); tile >= 0;
@@ -464,13 +464,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       // (they do not depend on the MMA, so they land while the mainloop runs)
       const int ncv = TMAE ? min(BN / 32, (p.N - nb * BN + 31) / 32) : 0;
       uint8_t* wbuf = ebuf + (warp - 4) * C::EW_BYTES;
+      // residual buffers in flight per warp: three when there is no [hi | lo] split output
+      // (the lo staging space holds the third f32 tile), else two
+      const int nbuf = p.c2_split > 0 ? 2 : 3;
+      auto fbuf = [&](int b) { return wbuf + (b < 2 ? b * 4096 : 12288); };
       if constexpr (TMAE) {
         if (lane == 0) {
           bulk_wait_read0();   // the previous tile's stores have left these buffers
           const int wr0 = p.row0 + mb * TM + (PAIR ? (int)rank * BM : 0) + ew * 32;
-          for (int c = 0; c < 2 && c < ncv; ++c) {
-            mbar_expect_tx(&rbar[2 * (warp - 4) + c], 4096);
-            tma_load_3d(wbuf + c * 4096, &tmR, &rbar[2 * (warp - 4) + c], nb * BN + 32 * c, wr0, c_slot);
+          for (int c = 0; c < nbuf && c < ncv; ++c) {
+            mbar_expect_tx(&rbar[3 * (warp - 4) + c], 4096);
+            tma_load_3d(fbuf(c), &tmR, &rbar[3 * (warp - 4) + c], nb * BN + 32 * c, wr0, c_slot);
           }
         }
       }
@@ -748,16 +752,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
             for (int k = 0; k < 8; ++k) sq[k] = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < ncv; ++c) {
-              const int b = c & 1, c0 = 32 * c, n0 = nb * BN + c0;
+            for (int c = 0, b = 0; c < ncv; ++c, b = b + 1 == nbuf ? 0 : b + 1) {
+              const int h = c & 1, c0 = 32 * c, n0 = nb * BN + c0;
               float v[32];
               __syncwarp();
               tmem_ld32(tbase + c0, v);
-              mbar_wait(&rbar[2 * wi + b], (rph >> b) & 1);
+              mbar_wait(&rbar[3 * wi + b], (rph >> b) & 1);
               rph ^= 1u << b;
-              float4* fb = reinterpret_cast<float4*>(wbuf + b * 4096) + lane * 8;
-              uint4* hb = reinterpret_cast<uint4*>(wbuf + 8192 + b * 2048) + lane * 4;
-              uint4* lb = reinterpret_cast<uint4*>(wbuf + 8192 + (2 + b) * 2048) + lane * 4;
+              if (nbuf == 3 && c >= 2) {   // the bf16 staging buffer h was last stored by chunk c - 2
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
+              }
+              float4* fb = reinterpret_cast<float4*>(fbuf(b)) + lane * 8;
+              uint4* hb = reinterpret_cast<uint4*>(wbuf + 8192 + h * 2048) + lane * 4;
+              uint4* lb = reinterpret_cast<uint4*>(wbuf + 8192 + (2 + h) * 2048) + lane * 4;
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 const float4 r4 = fb[k ^ (lane & 7)];
@@ -790,16 +798,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               fence_async_smem();   // generic-proxy smem writes -> visible to the TMA engine
               __syncwarp();
               if (lane == 0) {
-                tma_store_3d(&tmC, wbuf + b * 4096, n0, wrow0, c_slot);
+                tma_store_3d(&tmC, fbuf(b), n0, wrow0, c_slot);
                 if (p.C2 != nullptr) {
-                  tma_store_3d(&tmC2, wbuf + 8192 + b * 2048, n0, wrow0, c_slot);
-                  if (split) tma_store_3d(&tmC2, wbuf + 8192 + (2 + b) * 2048, n0 + p.c2_split, wrow0, c_slot);
+                  tma_store_3d(&tmC2, wbuf + 8192 + h * 2048, n0, wrow0, c_slot);
+                  if (split) tma_store_3d(&tmC2, wbuf + 8192 + (2 + h) * 2048, n0 + p.c2_split, wrow0, c_slot);
                 }
                 bulk_commit();
-                if (c + 2 < ncv) {   // refill this buffer pair once the stores have read it
+                if (c + nbuf < ncv) {   // refill this buffer once its stores have read it
                   bulk_wait_read0();
-                  mbar_expect_tx(&rbar[2 * wi + b], 4096);
-                  tma_load_3d(wbuf + b * 4096, &tmR, &rbar[2 * wi + b], n0 + 64, wrow0, c_slot);
+                  mbar_expect_tx(&rbar[3 * wi + b], 4096);
+                  tma_load_3d(fbuf(b), &tmR, &rbar[3 * wi + b], n0 + 32 * nbuf, wrow0, c_slot);
                 }
               }
               if (p.ssq_out != nullptr && ((n0 & 63) == 32 || n0 + 32 >= p.N)) {
