@@ -759,6 +759,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
               tmem_ld32(tbase + c0, v);
               mbar_wait(&rbar[3 * wi + b], (rph >> b) & 1);
               rph ^= 1u << b;
+              // refill the previous chunk's buffer now: its stores have had this chunk's TMEM
+              // load and barrier wait to finish reading it
+              if (c >= 1 && lane == 0) {
+                const int pb = b == 0 ? nbuf - 1 : b - 1;
+                if (c - 1 + nbuf < ncv) {
+                  bulk_wait_read0();
+                  mbar_expect_tx(&rbar[3 * wi + pb], 4096);
+                  tma_load_3d(fbuf(pb), &tmR, &rbar[3 * wi + pb], n0 - 32 + 32 * nbuf, wrow0, c_slot);
+                }
+              }
               if (nbuf == 3 && c >= 2) {   // the bf16 staging buffer h was last stored by chunk c - 2
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 __syncwarp();
@@ -804,11 +814,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                   if (split) tma_store_3d(&tmC2, wbuf + 8192 + (2 + h) * 2048, n0 + p.c2_split, wrow0, c_slot);
                 }
                 bulk_commit();
-                if (c + nbuf < ncv) {   // refill this buffer once its stores have read it
-                  bulk_wait_read0();
-                  mbar_expect_tx(&rbar[3 * wi + b], 4096);
-                  tma_load_3d(fbuf(b), &tmR, &rbar[3 * wi + b], n0 + 32 * nbuf, wrow0, c_slot);
-                }
+
               }
               if (p.ssq_out != nullptr && ((n0 & 63) == 32 || n0 + 32 >= p.N)) {
                 const float t = ((sq[0] + sq[1]) + (sq[2] + sq[3])) + ((sq[4] + sq[5]) + (sq[6] + sq[7]));
