@@ -1,0 +1,89 @@
+"""The reference's acceptance criteria (pkg/tests/test_acceptance.py) restated
+on the device path. Criteria 2 (minimal grouping), 3 (step counts), 4 (exact
+delta rule), 6 (determinism), 8 (feature map) and 9 (container round trip)
+have direct ports in test_scheduler.py, test_gpu_parity.py, test_gpu_kernels.py
+and test_container.py; this file covers 1, 5 and 7 in the reference's terms."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from conftest import MID  # noqa: E402
+from fixtures import cli_tokens, conditioned_weights  # noqa: E402
+from test_gpu_kernels import BF16, F32, LIB, gemm_args, stream  # noqa: E402
+from paper_2506_05229_b200 import _lib  # noqa: E402
+from paper_2506_05229_b200.config import ModelConfig  # noqa: E402
+from paper_2506_05229_b200.engine import prepare_weights  # noqa: E402
+from paper_2506_05229_b200.executors import Session, run_diagonal, run_sequential  # noqa: E402
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_criterion_1_schedules_agree_across_segment_counts(dtype):
+    """armt tests/test_acceptance.py criterion 1 on the reference's default
+    config (8 layers): diagonal vs sequential at 1..32 segments. The reference
+    allows 1e-3 in f32; the device schedules agree BITWISE (every kernel is
+    member-lane independent)."""
+    cfg = ModelConfig(eps_assoc=1.0)
+    prep = prepare_weights(conditioned_weights(cfg), dtype)
+    for segments in (1, 2, 4, 8, 16, 32):
+        tokens = cli_tokens(cfg, segments * cfg.segment_size, seed=segments)
+        seq, _ = run_sequential(prep, cfg, tokens, dtype=dtype)
+        diag, trace = run_diagonal(prep, cfg, tokens, dtype=dtype)
+        assert np.isfinite(seq).all()
+        assert np.array_equal(seq, diag), (dtype, segments)
+        assert trace.steps_executed == segments + cfg.n_layers - 1
+
+
+@pytest.mark.parametrize("K", [256, 2048])
+def test_criterion_5_grouped_gemm_matches_looped_singles_bitwise(K):
+    """Criterion 5: a grouped launch over G members equals G single-member
+    launches bitwise, for G = 1..8 (tcgen05 path, per-member layers and slots)."""
+    torch.manual_seed(5)
+    M, N, L = 300, 512, 8
+    A = torch.randn(L, M, K, device="cuda").bfloat16()
+    B = (torch.randn(L, N, K, device="cuda") * 0.05).bfloat16()
+    for G in range(1, 9):
+        slots = [(3 * g + 1) % L for g in range(G)]
+        layers = [(5 * g + 2) % L for g in range(G)]
+        Cg = torch.zeros(G, M, N, device="cuda")
+        _lib.check(LIB.armt_gemm(gemm_args(G, M, N, K, A, B, Cg, BF16, F32, slots, layers, list(range(G))),
+                                 stream()), "grouped")
+        for g in range(G):
+            C1 = torch.zeros(1, M, N, device="cuda")
+            _lib.check(LIB.armt_gemm(gemm_args(1, M, N, K, A, B, C1, BF16, F32, [slots[g]], [layers[g]], [0]),
+                                     stream()), "single")
+            assert torch.equal(Cg[g], C1[0]), (G, g)
+
+
+def test_criterion_7_diagonal_beats_sequential_wall():
+    """Criterion 7: the diagonal schedule is faster than the sequential one in
+    wall time (reference: 64 segments of an 8-layer stack on 8 CPU threads).
+    Device: 4-layer d=256 stack, 32 segments, both schedules replayed from one
+    CUDA graph each, best of 5 interleaved runs timed with CUDA events."""
+    cfg = ModelConfig(**MID, eps_assoc=10.0)
+    prep = prepare_weights(conditioned_weights(cfg), "bf16")
+    n = 32 * cfg.segment_size
+    tokens = torch.as_tensor(cli_tokens(cfg, n, seed=17)).cuda()
+    sessions = {k: Session(prep, n, schedule=k) for k in ("sequential", "diagonal")}
+    outs = {}
+    for k, s in sessions.items():
+        s._load_ids(tokens)
+        s.warm()
+        outs[k] = s.forward().clone()
+    assert torch.equal(outs["sequential"], outs["diagonal"])
+    best = {k: float("inf") for k in sessions}
+    for _ in range(5):
+        for k, s in sessions.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            s.forward()
+            e1.record()
+            torch.cuda.synchronize()
+            best[k] = min(best[k], e0.elapsed_time(e1))
+    speedup = best["sequential"] / best["diagonal"]
+    assert speedup > 1.3, best
