@@ -319,6 +319,8 @@ int attention_pp(int G, const void* qkv, long long ld_qkv, long long qkv_stride,
                  long long ctx_stride, int T, int H, float scale, cudaStream_t s);
 int attention_tc(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx, long long ld_ctx,
                  long long ctx_stride, int T, int H, int dh, float scale, cudaStream_t s);
+int attention_pp128(int G, const void* qkv, long long ld_qkv, long long qkv_stride, void* ctx, long long ld_ctx,
+                    long long ctx_stride, int T, int H, float scale, cudaStream_t s);
 }
 using namespace armt;
 
@@ -341,15 +343,15 @@ extern "C" int armt_attention(int G, const void* qkv, long long ld_qkv, long lon
   }
   ARMT_REQUIRE(dh % 8 == 0 && ld_qkv % 8 == 0 && ld_ctx % 2 == 0, ARMT_ERR_DIM,
                "attention bf16: head dim and row strides must be multiples of 8");
-  // tcgen05 kernels: ping-pong pairs for d_head 64, one tile per CTA for 128
+  // tcgen05 kernels: ping-pong pairs for d_head 64 and 128
   // (ARMT_ATTN=mma forces the mma.sync kernel, ARMT_ATTN=tc the single-tile
-  // tcgen05 kernel at d_head 64, for A/B runs)
-  static const char force = [] {
-    const char* e = getenv("ARMT_ATTN");
-    return e != nullptr ? e[0] : '\0';
-  }();
+  // tcgen05 kernel, for A/B runs)
+  const char* force_env = getenv("ARMT_ATTN");   // read per call: tests switch kernels in one process
+  const char force = force_env != nullptr ? force_env[0] : '\0';
   if (dh == 64 && force != 'm' && force != 't')
     return attention_pp(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, scale, s);
+  if (dh == 128 && force != 'm' && force != 't')
+    return attention_pp128(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, scale, s);
   if ((dh == 64 || dh == 128) && force != 'm')
     return attention_tc(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);
   if (dh <= 16) return launch_bf16<16>(G, qkv, ld_qkv, qkv_stride, ctx, ld_ctx, ctx_stride, T, H, dh, scale, s);

@@ -211,6 +211,27 @@ def test_attention_dh64_pairs_and_lazy_rescale(T, amp, G, H):
     assert rel(ctx.float(), want) < 1e-2
 
 
+@pytest.mark.parametrize("T", [64, 300, 1152])
+@pytest.mark.parametrize("amp", [1.0, 6.0])
+@pytest.mark.parametrize("G,H", [(3, 2), (1, 3), (2, 32)])
+def test_attention_dh128_pairs_and_lazy_rescale(T, amp, G, H, monkeypatch):
+    # d_head 128 runs the ping-pong kernel on 64-key steps (C5's head size): odd / even /
+    # single query-tile counts, a ragged tail, large scores forcing O rescales, and the
+    # single-tile tcgen05 kernel (ARMT_ATTN=tc) as a second check
+    torch.manual_seed(8)
+    dh = 128
+    d = H * dh
+    qkv = (amp * torch.randn(G, T, 3 * d, device=DEV)).to(torch.bfloat16)
+    want = attention_ref(qkv.float(), H, dh)
+    for force in (None, "tc"):
+        if force:
+            monkeypatch.setenv("ARMT_ATTN", force)
+        ctx = torch.zeros(G, T, d, device=DEV, dtype=torch.bfloat16)
+        _lib.check(LIB.armt_attention(G, qkv.data_ptr(), 3 * d, T * 3 * d, ctx.data_ptr(), d, T * d, BF16, T, H,
+                                      dh, 1.0 / math.sqrt(dh), stream()), "attention")
+        assert rel(ctx.float(), want) < 1e-2, force
+
+
 def test_dpfp_known_answers_on_device():
     # pkg/tests/test_memory.py:25-33 pinned on the device feature map
     from paper_2506_05229_b200.layers import dpfp
