@@ -24,7 +24,7 @@ using namespace tcx;
 
 constexpr int DH = 128, BQ = 128, BKV = 64, NG = 2, NTHREADS = 128 + NG * 128;
 #ifndef ARMT_PP128_NST
-#define ARMT_PP128_NST 3
+#define ARMT_PP128_NST 4
 #endif
 constexpr int NST = ARMT_PP128_NST;               // K/V stages
 constexpr int QTILE = BQ * DH * 2;                // 32 KB: two 64-column sub-tiles
@@ -35,7 +35,11 @@ constexpr int Q_BYTES = NG * QTILE;               // one Q buffer (three tiles)
 constexpr int KV_BYTES = 2 * KVTILE;              // K + V of one stage
 constexpr int S_COL = 0, O_COL = NG * BKV, P_COL = O_COL + NG * DH, TMEM_COLS = 512;
 constexpr int BAR_BYTES = 512;
-constexpr int SMEM = 2 * Q_BYTES + NST * KV_BYTES + BAR_BYTES;
+#ifndef ARMT_PP128_QB
+#define ARMT_PP128_QB 1
+#endif
+constexpr int QB = ARMT_PP128_QB;                 // Q buffers (items in flight)
+constexpr int SMEM = QB * Q_BYTES + NST * KV_BYTES + BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "attention (d_head 128) shared memory budget");
 static_assert(P_COL + NG * BKV / 2 <= TMEM_COLS, "TMEM columns");
 constexpr float RESCALE_LOG2 = 8.f;
@@ -148,7 +152,7 @@ attn_pp128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 operand tiles need 1 KB alignment
   uint8_t* sQ = smem;                              // buffer qi: tile s at qi * Q_BYTES + s * QTILE
-  uint8_t* sKV = sQ + 2 * Q_BYTES;                 // stage st: K at st * KV_BYTES, V at + KVTILE
+  uint8_t* sKV = sQ + QB * Q_BYTES;                // stage st: K at st * KV_BYTES, V at + KVTILE
   uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + NST * KV_BYTES);
   uint64_t* q_full = bar;                    // [2]
   uint64_t* q_empty = bar + 2;               // [2]
@@ -198,8 +202,8 @@ attn_pp128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       int tt = 0, it = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
         const Item I = decode(w, p);
-        const int qi = it & 1;
-        mbar_wait_sleep(&q_empty[qi], ((it >> 1) & 1) ^ 1);
+        const int qi = it % QB;
+        mbar_wait_sleep(&q_empty[qi], ((it / QB) & 1) ^ 1);
         int nvalid = 0;
 #pragma unroll
         for (int s = 0; s < NG; ++s) nvalid += I.n[s] > 0;
@@ -250,8 +254,8 @@ attn_pp128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       };
       for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
         const Item I = decode(w, p);
-        const int qi = it & 1;
-        mbar_wait(&q_full[qi], (it >> 1) & 1);
+        const int qi = it % QB;
+        mbar_wait(&q_full[qi], (it / QB) & 1);
         for (int j = 0; j < I.nmax; ++j) {
           const int st = (tt + j) % NST;
           mbar_wait(&kv_full[st], ((tt + j) / NST) & 1);
