@@ -86,4 +86,6 @@ def test_criterion_7_diagonal_beats_sequential_wall():
             torch.cuda.synchronize()
             best[k] = min(best[k], e0.elapsed_time(e1))
     speedup = best["sequential"] / best["diagonal"]
+    print(f"criterion 7 (device): sequential {best['sequential']:.2f} ms, diagonal {best['diagonal']:.2f} ms, "
+          f"speedup {speedup:.2f}")
     assert speedup > 1.3, best
