@@ -43,11 +43,15 @@ constexpr int SMEM = QB * Q_BYTES + NST * KV_BYTES + BAR_BYTES;
 static_assert(SMEM <= 227 * 1024, "attention (d_head 128) shared memory budget");
 static_assert(P_COL + NG * BKV / 2 <= TMEM_COLS, "TMEM columns");
 constexpr float RESCALE_LOG2 = 8.f;
+#ifndef ARMT_PP128_CHUNKED
+#define ARMT_PP128_CHUNKED 1
+#endif
+constexpr bool CHUNKED = ARMT_PP128_CHUNKED;
 
 struct Params {
   __nv_bfloat16* ctx;
   long long ld_ctx, ctx_stride;
-  int T, H, G, d, nq, npair, nkv_all;
+  int T, H, G, d, nq, npair, nkv_all, nctas, chunked_items;
   float scale_log2;
 };
 
@@ -127,13 +131,29 @@ struct Item {
 // (member, head) slots of a round are visited in alternating directions (K/V reuse in L2)
 __device__ __forceinline__ Item decode(int w, const Params& p) {
   Item I;
-  const int HG = p.H * p.G;
-  const int round = w / HG;
+  const int HG = p.H * p.G, P = p.nctas;
+  int round, slot;
+  if (CHUNKED && w < p.chunked_items) {
+    // chunks of P (member, head) slots, all query-pair rounds of a chunk together, heaviest
+    // first: with the persistent round-robin CTA b takes slot chunk * P + b in every round, so
+    // each CTA walks one slot's query pairs back to back (its K/V stays in L2) and every CTA
+    // gets the same work per chunk
+    const int per = P * p.npair;
+    const int c = w / per, x = w - c * per;
+    round = x / P;
+    slot = c * P + (x - round * P);
+  } else {
+    // the slots past the last whole chunk: rounds over all of them, alternating direction
+    const int base = CHUNKED ? p.chunked_items / p.npair : 0, n = HG - base;
+    const int x = w - (CHUNKED ? p.chunked_items : 0);
+    round = x / n;
+    int r = x - round * n;
+    if (round & 1) r = n - 1 - r;
+    slot = base + r;
+  }
   const int trip = p.npair - 1 - round;
-  int rem = w - round * HG;
-  if (round & 1) rem = HG - 1 - rem;
-  I.h = rem % p.H;
-  I.g = rem / p.H;
+  I.h = slot % p.H;
+  I.g = slot / p.H;
   I.nmax = 0;
 #pragma unroll
   for (int s = 0; s < NG; ++s) {
@@ -427,6 +447,8 @@ int attention_pp128(int G, const void* qkv, long long ld_qkv, long long qkv_stri
   }
   const int items = p.npair * H * G;
   const int grid = items < num_sms() ? items : num_sms();
+  p.nctas = grid;
+  p.chunked_items = ((H * G) / grid) * grid * p.npair;
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(grid);
